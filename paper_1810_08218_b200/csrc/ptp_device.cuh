@@ -1,0 +1,142 @@
+// Device-side types and helpers of the B200 PTP solver (sm_100a).
+//
+// Data layout in HBM (per mesh, built once by pack_fans_kernel):
+//   cptr[n+1]            corner offsets, original vertex order (int32)
+//   ring[cptr[n]+n]      fan ring per vertex at cptr[v]+v: r_0..r_d (int32);
+//                        corner c of v is (ring[c], ring[c+1]); bit 31 of
+//                        ring[cptr[v]+v+c] flags corner c as degenerate
+//                        (update_kernel.hpp:51-57 test precomputed)
+//   ringL<T>[..]         |x| = sqrt(dot(x,x)) per ring entry, x = p[r]-p[v] in T
+//   quad<T>[4*cptr[n]]   per corner {q11, q12, q22, a} of the Gram inverse
+//                        (update_kernel.hpp:55-60), computed in T with the
+//                        reference's operation order (no FMA)
+// Per query (per group of CTAs):
+//   dist0/dist1<T>[n]    Jacobi double buffer (ptp.cpp:61-63), original order
+//   lab0/lab1[n]         nearest-source labels (multi-source runs only)
+//   level[n]             BFS level (-1 = unvisited), fused topleset discovery
+//   queue[n]             vertices in BFS order, level r at [limits[r], limits[r+1])
+//   limits[n+2]
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gdb {
+
+constexpr int kBlock = 512;        // threads per CTA
+constexpr int kW = 8;              // lanes per vertex (sub-warp): 7 corners per pass
+constexpr unsigned kFull = 0xffffffffu;
+
+// One group of CTAs runs one query; its control block lives in global memory.
+// Hot words sit on separate 128-byte lines.
+struct alignas(128) GroupCtl {
+    unsigned int bar;              // barrier arrivals (monotonic within a launch)
+    unsigned int pad0[31];
+    unsigned long long slot[3];    // per-iteration max relative change (bit pattern)
+    unsigned long long pad1[13];
+    int tail;                      // BFS queue tail (= limits[top+1])
+    int err;
+    int pad2[30];
+    // loop state, saved by CTA 0 of the group when a launch ends mid-run
+    int k, i, rho, parity, retired, bfs_open, done, initialized;
+    int s_tail, s_limk, s_bb, s_fe, s_frzb, s_frze, pad3[2];
+    unsigned long long relax, degen, updates;
+    unsigned long long pad4[5];
+    // FPS / argmax scratch: per-CTA (value bits, index)
+};
+
+struct QueryStats {  // per query, written by CTA 0 of the group
+    long long relax, degen, updates;
+    int iterations, rho, unreached, done;
+    double radius;
+    int argmax, pad;
+};
+
+struct TraceRow {  // mirrors geodist_band_row
+    int k, i, j, conv;
+    long long updated;
+    double max_rel;
+};
+
+struct MeshDev {
+    const int* cptr;
+    const int* ring;
+    const void* ringL;
+    const void* quad;
+    int n;
+};
+
+struct RunArgs {
+    MeshDev mesh;
+    // per-group buffers: group g at base + g * stride (elements)
+    void* dist0;
+    void* dist1;
+    int* lab0;
+    int* lab1;
+    int* level;
+    int* queue;
+    int* limits;
+    long long stride;
+    GroupCtl* ctl;
+    int groups;
+    int blocks_per_group;
+    // queries
+    const int* src;      // concatenated sources (caller order)
+    const int* src_off;  // nq+1 offsets, or NULL with src_count
+    int src_count;       // sources of query 0 when src_off == NULL (FPS round)
+    int nq;
+    double eps;
+    int fused_bfs;       // 0: queue/limits preloaded (caller ordering), rho = given_rho
+    int given_rho;
+    int phase_init;      // start a fresh query (else resume from ctl state)
+    int max_iters;       // iterations per launch (<= 0: run to completion)
+    // diagnostics
+    TraceRow* trace;     // rows indexed by (k - trace_k0), capacity trace_cap
+    int trace_k0;
+    int trace_cap;
+    int* last_change;    // n, or NULL
+    // outputs (query q at + q*n)
+    void* out_dist;
+    int out_double;      // out_dist element: 1 double, 0 float
+    int* out_labels;     // or NULL
+    QueryStats* qstats;  // nq rows
+    // FPS: argmax over the final field, appended to src[src_count]
+    int fps_mode;
+    unsigned long long* fps_scratch;  // 2 * gridDim.x words
+    int* fps_samples;                 // device sample list (== src)
+    int fps_final;
+};
+
+__device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
+__device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T> struct Lim;
+template <> struct Lim<float> {
+    __device__ static float inf() { return __int_as_float(0x7f800000); }
+    __device__ static float min_normal() { return 1.17549435e-38f; }  // FLT_MIN
+    __device__ static unsigned long long bits(float x) {
+        return static_cast<unsigned long long>(__float_as_uint(x));
+    }
+    __device__ static float from_bits(unsigned long long b) {
+        return __uint_as_float(static_cast<unsigned>(b));
+    }
+};
+template <> struct Lim<double> {
+    __device__ static double inf() { return __longlong_as_double(0x7ff0000000000000LL); }
+    __device__ static double min_normal() { return 2.2250738585072014e-308; }  // DBL_MIN
+    __device__ static unsigned long long bits(double x) {
+        return static_cast<unsigned long long>(__double_as_longlong(x));
+    }
+    __device__ static double from_bits(unsigned long long b) {
+        return __longlong_as_double(static_cast<long long>(b));
+    }
+};
+
+}  // namespace gdb

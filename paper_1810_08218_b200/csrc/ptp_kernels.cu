@@ -1,0 +1,785 @@
+// B200 (sm_100a) kernels of the PTP geodesic solver.
+//
+//   pack_kernel<T>      one-time per mesh & precision: per-ring |x| and per-corner
+//                       Gram inverse {q11,q12,q22,a} + degenerate flag, i.e. the
+//                       geometry-only half of planar_update<T>
+//                       (reference include/geodist/update_kernel.hpp:38-60)
+//   ptp_run_kernel<T,L> persistent cooperative kernel; one group of CTAs per
+//                       query.  Per query: reset, seed sources (ptp.cpp:61-73),
+//                       then the band loop of run_impl<T> (ptp.cpp:79-132) with
+//                         * the BFS of compute_toplesets (toplesets.cpp:37-55)
+//                           fused in: level k+1 is discovered while level k is
+//                           relaxed (one group barrier per iteration serves both)
+//                         * relax_vertex (update_kernel.hpp:93-120): 8 lanes per
+//                           vertex, one corner per lane, lexicographic
+//                           (value, corner) shuffle-min = the strict '<' scan
+//                         * the front max relative change (ptp.cpp:107) reduced
+//                           into the barrier; retirement + freeze (ptp.cpp:114-131)
+//                           decided identically by every CTA after the barrier
+//                       then copy-out (ptp.cpp:139-147), optional FPS argmax
+//                       (sampling.cpp:29-36).
+//   planar_test_kernel  planar_update<T> on raw inputs (parity hook).
+//
+// All floating point goes through __f*_rn / __d*_rn intrinsics: IEEE rounding,
+// no FMA contraction, the reference's left-to-right association -- the CPU
+// reference build has no FMA, so results are bit-identical.
+#include <climits>
+#include <cstdio>
+
+#include "ptp_device.cuh"
+#include "ptp_launch.hpp"
+
+namespace gdb {
+
+// ---------------------------------------------------------------------------
+// exact arithmetic helpers
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float dv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double dv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sq(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sq(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float fab(float a) { return fabsf(a); }
+__device__ __forceinline__ double fab(double a) { return fabs(a); }
+
+template <typename T> __device__ __forceinline__ T to_t(double x);
+template <> __device__ __forceinline__ float to_t<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double to_t<double>(double x) { return x; }
+
+// dot in Vec3T<T> order: (x*x + y*y) + z*z   (vec3.hpp:21-24)
+template <typename T>
+__device__ __forceinline__ T dot3(T ax, T ay, T az, T bx, T by, T bz) {
+    return add(add(mul(ax, bx), mul(ay, by)), mul(az, bz));
+}
+
+// Geometry-only part of planar_update (update_kernel.hpp:51-60).
+template <typename T>
+__device__ __forceinline__ bool corner_geometry(T g11, T g22, T g12, T& q11, T& q12, T& q22,
+                                                T& a) {
+    const T det = sub(mul(g11, g22), mul(g12, g12));
+    const T sin_tol = T(1e-12);
+    const T thr = mul(mul(mul(sin_tol, sin_tol), g11), g22);
+    if (!(det > thr)) {
+        q11 = q12 = q22 = a = T(0);
+        return true;  // degenerate: fallback only
+    }
+    q11 = dv(g22, det);
+    q22 = dv(g11, det);
+    q12 = dv(-g12, det);
+    a = add(add(q11, mul(T(2), q12)), q22);
+    return false;
+}
+
+// Value-dependent part of planar_update (update_kernel.hpp:38-50, 61-78) plus
+// the mixed-label restriction of relax_vertex (update_kernel.hpp:103-111),
+// which reduces to the one-sided candidate with side chosen by f1 <= f2.
+template <typename T>
+__device__ __forceinline__ T corner_candidate(T t1, T t2, T L1, T L2, T q11, T q12, T q22, T a,
+                                              bool degen_geom, bool mixed, int& side, int& deg) {
+    const T inf = Lim<T>::inf();
+    const T f1 = add(t1, L1);
+    const T f2 = add(t2, L2);
+    T val;
+    if (f1 <= f2) {
+        val = f1;
+        side = 0;
+    } else {
+        val = f2;
+        side = 1;
+    }
+    deg = 0;
+    if (t1 == inf && t2 == inf) {
+        side = -1;
+        return inf;
+    }
+    if (t1 == inf || t2 == inf || mixed) return val;
+    if (degen_geom) {
+        deg = 1;
+        return val;
+    }
+    const T qt1 = add(mul(q11, t1), mul(q12, t2));
+    const T qt2 = add(mul(q12, t1), mul(q22, t2));
+    const T b = mul(T(-2), add(qt1, qt2));
+    const T c = sub(add(mul(t1, qt1), mul(t2, qt2)), T(1));
+    const T disc = sub(mul(b, b), mul(mul(T(4), a), c));
+    if (disc >= T(0)) {
+        const T p = dv(add(-b, sq(disc)), mul(T(2), a));
+        const T tmax = t1 < t2 ? t2 : t1;
+        if (p >= tmax) {
+            const T m1 = add(mul(q11, sub(t1, p)), mul(q12, sub(t2, p)));
+            const T m2 = add(mul(q12, sub(t1, p)), mul(q22, sub(t2, p)));
+            if (m1 < T(0) && m2 < T(0) && p <= val) {
+                val = p;
+                side = t1 <= t2 ? 0 : 1;
+            }
+        }
+    }
+    return val;
+}
+
+// relative_change (ptp.cpp:37-43)
+template <typename T>
+__device__ __forceinline__ T rel_change(T before, T after) {
+    const T inf = Lim<T>::inf();
+    if (before == inf) return after == inf ? T(0) : inf;
+    const T denom = before == T(0) ? Lim<T>::min_normal() : before;
+    return dv(fab(sub(after, before)), denom);
+}
+
+template <typename T> struct Quad;
+template <> struct Quad<float> {
+    float q11, q12, q22, a;
+    __device__ __forceinline__ void load(const void* base, int c) {
+        const float4 v = __ldg(static_cast<const float4*>(base) + c);
+        q11 = v.x; q12 = v.y; q22 = v.z; a = v.w;
+    }
+    __device__ __forceinline__ static void store(void* base, int c, float x, float y, float z,
+                                                 float w) {
+        static_cast<float4*>(base)[c] = make_float4(x, y, z, w);
+    }
+};
+template <> struct Quad<double> {
+    double q11, q12, q22, a;
+    __device__ __forceinline__ void load(const void* base, int c) {
+        const double2* p = static_cast<const double2*>(base) + 2 * static_cast<size_t>(c);
+        const double2 u = __ldg(p), w = __ldg(p + 1);
+        q11 = u.x; q12 = u.y; q22 = w.x; a = w.y;
+    }
+    __device__ __forceinline__ static void store(void* base, int c, double x, double y, double z,
+                                                 double w) {
+        double2* p = static_cast<double2*>(base) + 2 * static_cast<size_t>(c);
+        p[0] = make_double2(x, y);
+        p[1] = make_double2(z, w);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// one-time geometry pack (per mesh, per precision)
+template <typename T>
+__global__ void pack_kernel(const double* __restrict__ xyz, int n, const int* __restrict__ cptr,
+                            const int* __restrict__ ring_in, int* __restrict__ ring_out,
+                            T* __restrict__ ringL, void* __restrict__ quad) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int c0 = cptr[v], d = cptr[v + 1] - c0, r0 = c0 + v;
+    if (d == 0) {
+        ring_out[r0] = ring_in[r0];
+        ringL[r0] = T(0);
+        return;
+    }
+    const T px = to_t<T>(xyz[3 * (size_t)v]), py = to_t<T>(xyz[3 * (size_t)v + 1]),
+            pz = to_t<T>(xyz[3 * (size_t)v + 2]);
+    T x0 = 0, y0 = 0, z0 = 0, g0 = 0;  // ring entry e-1
+    for (int e = 0; e <= d; ++e) {
+        const int r = ring_in[r0 + e];
+        const T x = sub(to_t<T>(xyz[3 * (size_t)r]), px);
+        const T y = sub(to_t<T>(xyz[3 * (size_t)r + 1]), py);
+        const T z = sub(to_t<T>(xyz[3 * (size_t)r + 2]), pz);
+        const T g = dot3(x, y, z, x, y, z);
+        ringL[r0 + e] = sq(g);  // norm(x) = sqrt(dot(x, x)) (vec3.hpp:31-34)
+        ring_out[r0 + e] = r;
+        if (e > 0) {
+            const int c = e - 1;  // corner (ring[c], ring[c+1])
+            const T g12 = dot3(x0, y0, z0, x, y, z);
+            T q11, q12, q22, a;
+            const bool degen = corner_geometry(g0, g, g12, q11, q12, q22, a);
+            Quad<T>::store(quad, c0 + c, q11, q12, q22, a);
+            if (degen) ring_out[r0 + c] = ring_in[r0 + c] | INT_MIN;
+        }
+        x0 = x; y0 = y; z0 = z; g0 = g;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// group barrier: all CTAs of one group; thread 0 runs `post` after release
+template <typename Post>
+__device__ __forceinline__ void group_barrier(unsigned* bar, unsigned& epoch, unsigned nblk,
+                                              Post&& post) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ++epoch;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        const unsigned target = epoch * nblk;
+        while (static_cast<int>(ld_acquire(bar) - target) < 0) {
+        }
+        __threadfence();
+        post();
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T block_max(T x, T* red) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const T y = __shfl_xor_sync(kFull, x, o);
+        x = y > x ? y : x;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    T r = T(0);
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : T(0);
+        for (int o = 16; o > 0; o >>= 1) {
+            const T y = __shfl_xor_sync(kFull, r, o);
+            r = y > r ? y : r;
+        }
+    }
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+__device__ __forceinline__ long long block_sum(long long x, long long* red) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    long long r = 0;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+    }
+    __syncthreads();
+    return r;
+}
+
+struct Bcast {
+    int k, i, j, bb, fe, be, expb, expe, frzb, frze, parity, done;
+};
+
+// Relax one band vertex per sub-warp (all 32 lanes of the warp call this in
+// lock-step; `act` predicates the sub-warp).  Fused BFS: lanes holding ring
+// ids of a level-k vertex claim unvisited neighbours for level k+1.
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax_sub(const MeshDev& M, const int* __restrict__ ring,
+                                          const T* __restrict__ ringL, bool act, int p, int kk,
+                                          const int* queue, const T* dp, T* dc, const int* lp,
+                                          int* lc, int fe, bool expand, int* level, int* queue_w,
+                                          int* tail_ptr, T eps, int* last_change, T& my_max,
+                                          long long& calls, long long& degs) {
+    const T inf = Lim<T>::inf();
+    const int lane = threadIdx.x & (kW - 1);
+    int v = 0, c0 = 0, d = 0;
+    if (act) {
+        v = ldcg(queue + p);
+        c0 = __ldg(M.cptr + v);
+        d = __ldg(M.cptr + v + 1) - c0;
+    }
+    const int r0 = c0 + v;
+    const T tv = act ? ldcg(dp + v) : inf;
+    int lv = -1;
+    if (LABELS && act) lv = ldcg(lp + v);
+    int nch = d > 0 ? (d + kW - 2) / (kW - 1) : 0;
+    nch = __reduce_max_sync(kFull, nch);
+    T best = lane == 0 ? tv : inf;
+    int bidx = lane == 0 ? -1 : INT_MAX;
+    int blab = lane == 0 ? lv : -1;
+    const bool exp = act && expand;
+    for (int ch = 0; ch < nch; ++ch) {
+        const int e = ch * (kW - 1) + lane;  // ring entry == corner index
+        const bool has = act && d > 0 && e <= d;
+        int rid = 0;
+        T L = T(0), t = inf;
+        int l = -1;
+        if (has) {
+            rid = __ldg(ring + r0 + e);
+            L = __ldg(ringL + r0 + e);
+        }
+        const int id = rid & INT_MAX;
+        if (has) {
+            t = ldcg(dp + id);
+            if (LABELS) l = ldcg(lp + id);
+        }
+        const T t2 = __shfl_down_sync(kFull, t, 1, kW);
+        const T L2 = __shfl_down_sync(kFull, L, 1, kW);
+        int l2 = -1;
+        if (LABELS) l2 = __shfl_down_sync(kFull, l, 1, kW);
+        if (has && lane < kW - 1 && e < d) {
+            Quad<T> q;
+            q.load(M.quad, c0 + e);
+            const bool mixed = LABELS && l != l2 && t != inf && t2 != inf;
+            int side, deg;
+            const T val = corner_candidate(t, t2, L, L2, q.q11, q.q12, q.q22, q.a, rid < 0, mixed,
+                                           side, deg);
+            degs += deg;
+            if (val < best) {
+                best = val;
+                bidx = e;
+                if (LABELS) blab = side == 0 ? l : l2;
+            }
+        }
+        // fused BFS expansion (toplesets.cpp:44-52)
+        bool claim = false;
+        if (exp && has) {
+            if (ldcg(level + id) < 0) claim = atomicCAS(level + id, -1, kk + 1) == -1;
+        }
+        const unsigned bal = __ballot_sync(kFull, claim);
+        if (bal) {
+            const int l32 = threadIdx.x & 31;
+            const int leader = __ffs(bal) - 1;
+            int base = 0;
+            if (l32 == leader) base = atomicAdd(tail_ptr, __popc(bal));
+            base = __shfl_sync(kFull, base, leader);
+            if (claim) queue_w[base + __popc(bal & ((1u << l32) - 1u))] = id;
+        }
+    }
+    // lexicographic (value, corner) min over the sub-warp == first strict-'<' winner
+    for (int o = kW / 2; o > 0; o >>= 1) {
+        const T ob = __shfl_xor_sync(kFull, best, o, kW);
+        const int oi = __shfl_xor_sync(kFull, bidx, o, kW);
+        int ol = -1;
+        if (LABELS) ol = __shfl_xor_sync(kFull, blab, o, kW);
+        if (ob < best || (ob == best && oi < bidx)) {
+            best = ob;
+            bidx = oi;
+            if (LABELS) blab = ol;
+        }
+    }
+    if (act && lane == 0) {
+        dc[v] = best;
+        if (LABELS) lc[v] = blab;
+        calls += d;
+        const T rc = rel_change(tv, best);
+        if (p < fe && rc > my_max) my_max = rc;
+        if (last_change != nullptr && rc >= eps) last_change[v] = kk;
+    }
+}
+
+template <typename T, bool LABELS>
+__global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
+    __shared__ Bcast S;
+    __shared__ T red_t[kBlock / 32];
+    __shared__ long long red_l[kBlock / 32];
+    __shared__ double red_v[kBlock / 32];
+    __shared__ int red_i[kBlock / 32];
+
+    const int tid = threadIdx.x;
+    const int nb = A.blocks_per_group;
+    const int g = blockIdx.x / nb;
+    const int lb = blockIdx.x - g * nb;
+    GroupCtl* ctl = A.ctl + g;
+    const long long off = static_cast<long long>(g) * A.stride;
+    T* dist[2] = {static_cast<T*>(A.dist0) + off, static_cast<T*>(A.dist1) + off};
+    int* lab[2] = {nullptr, nullptr};
+    if (LABELS) {
+        lab[0] = A.lab0 + off;
+        lab[1] = A.lab1 + off;
+    }
+    int* level = A.level + off;
+    int* queue = A.queue + off;
+    int* limits = A.limits + off;
+    const MeshDev M = A.mesh;
+    const int n = M.n;
+    const int* ring = M.ring;
+    const T* ringL = static_cast<const T*>(M.ringL);
+    const T inf = Lim<T>::inf();
+    const T eps = static_cast<T>(A.eps);
+    unsigned epoch = 0;
+    const int gthreads = nb * kBlock;
+    const int gtid = lb * kBlock + tid;
+
+    for (int q = g; q < A.nq; q += A.groups) {
+        const int s0 = A.src_off ? A.src_off[q] : 0;
+        const int m = A.src_off ? A.src_off[q + 1] - s0 : A.src_count;
+        const int* src = A.src + s0;
+        // thread-0 loop state (identical in every CTA of the group)
+        int k = 0, i = 1, rho = INT_MAX, parity = 0, bfs_open = 0, done = 0;
+        int tail = 0, limk = 0, bb = 0, fe = 0, frzb = 0, frze = 0;
+        unsigned long long upd = 0;
+
+        if (A.phase_init) {
+            // reset (ptp.cpp:61-68)
+            for (int v = gtid; v < n; v += gthreads) {
+                dist[0][v] = inf;
+                dist[1][v] = inf;
+                if (LABELS) {
+                    lab[0][v] = -1;
+                    lab[1][v] = -1;
+                }
+                if (A.fused_bfs) level[v] = -1;
+                if (A.last_change) A.last_change[v] = 0;
+            }
+            if (gtid == 0) {
+                ctl->relax = ctl->degen = ctl->updates = 0;
+                ctl->slot[0] = ctl->slot[1] = ctl->slot[2] = 0ull;
+                ctl->tail = m;
+                ctl->err = 0;
+            }
+            group_barrier(&ctl->bar, epoch, nb, [] {});
+            // seed sources: d = 0, label = index in caller order (ptp.cpp:69-73)
+            for (int s = gtid; s < m; s += gthreads) {
+                const int v = src[s];
+                dist[0][v] = T(0);
+                dist[1][v] = T(0);
+                if (LABELS) {
+                    lab[0][v] = s;
+                    lab[1][v] = s;
+                }
+                if (A.fused_bfs) {
+                    level[v] = 0;
+                    queue[s] = v;
+                }
+            }
+            if (A.fused_bfs && gtid == 0) {
+                limits[0] = 0;
+                limits[1] = m;
+            }
+            group_barrier(&ctl->bar, epoch, nb, [] {});
+            if (A.fused_bfs) {
+                // iteration 0: level 0 -> level 1
+                const int sw = tid / kW;
+                const int stride = nb * (kBlock / kW);
+                T dummy_max = T(0);
+                long long dc0 = 0, dd0 = 0;
+                for (int t = lb + nb * sw;; t += stride) {
+                    const bool act = t < m;
+                    if (!__any_sync(kFull, act)) break;
+                    // expansion only: relax of a source is skipped (sources are never
+                    // in a band); reuse the sub-warp ring walk with writes disabled
+                    const int lane = tid & (kW - 1);
+                    int v = 0, c0 = 0, d = 0;
+                    if (act) {
+                        v = ldcg(queue + t);
+                        c0 = __ldg(M.cptr + v);
+                        d = __ldg(M.cptr + v + 1) - c0;
+                    }
+                    int nch = d > 0 ? (d + kW) / kW : 0;  // ring entries 0..d
+                    nch = __reduce_max_sync(kFull, nch);
+                    for (int ch = 0; ch < nch; ++ch) {
+                        const int e = ch * kW + lane;
+                        bool claim = false;
+                        int id = 0;
+                        if (act && d > 0 && e <= d) {
+                            id = __ldg(ring + c0 + v + e) & INT_MAX;
+                            if (ldcg(level + id) < 0) claim = atomicCAS(level + id, -1, 1) == -1;
+                        }
+                        const unsigned bal = __ballot_sync(kFull, claim);
+                        if (bal) {
+                            const int l32 = tid & 31;
+                            const int leader = __ffs(bal) - 1;
+                            int base = 0;
+                            if (l32 == leader) base = atomicAdd(&ctl->tail, __popc(bal));
+                            base = __shfl_sync(kFull, base, leader);
+                            if (claim) queue[base + __popc(bal & ((1u << l32) - 1u))] = id;
+                        }
+                    }
+                }
+                (void)dummy_max; (void)dc0; (void)dd0;
+            }
+            group_barrier(&ctl->bar, epoch, nb, [&] {
+                if (A.fused_bfs) {
+                    const int t = ldcg(&ctl->tail);
+                    tail = t;
+                    limk = m;
+                    bb = m;
+                    fe = t;
+                    if (t == m) {
+                        bfs_open = 0;
+                        rho = 1;
+                    } else {
+                        bfs_open = 1;
+                        if (lb == 0) limits[2] = t;
+                    }
+                } else {
+                    rho = A.given_rho;
+                    bfs_open = 0;
+                    tail = ldcg(limits + rho);
+                    bb = ldcg(limits + 1);
+                    fe = rho >= 2 ? ldcg(limits + 2) : tail;
+                }
+                done = !bfs_open && i > rho - 1;
+            });
+        } else if (tid == 0) {
+            // resume
+            k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
+            bfs_open = ctl->bfs_open; done = ctl->done;
+            tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
+            frzb = ctl->s_frzb; frze = ctl->s_frze;
+        }
+
+        T my_max = T(0);
+        long long calls = 0, degs = 0;
+        int iters = 0;
+        int pf = -1;
+        for (;;) {
+            if (tid == 0) {
+                const bool stop = done || (A.max_iters > 0 && iters >= A.max_iters);
+                S.done = stop ? 1 : 0;
+                if (!stop) {
+                    const int kk = k + 1;
+                    const int j = bfs_open ? kk : min(kk, rho - 1);
+                    S.k = kk;
+                    S.i = i;
+                    S.j = j;
+                    S.bb = bb;
+                    S.fe = fe;
+                    S.be = (bfs_open || j + 1 == rho) ? tail : ldcg(limits + j + 1);
+                    S.expb = bfs_open ? limk : 0;
+                    S.expe = bfs_open ? tail : 0;
+                    S.frzb = frzb;
+                    S.frze = frze;
+                    S.parity = parity;
+                    pf = -1;
+                    if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
+                        pf = (bfs_open && i + 2 == kk + 1) ? tail : ldcg(limits + i + 2);
+                    if (lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
+                }
+            }
+            __syncthreads();
+            if (S.done) break;
+            const int kk = S.k;
+            const int prv = S.parity, cur = prv ^ 1;
+            const T* dp = dist[prv];
+            T* dcur = dist[cur];
+            const int* lp = LABELS ? lab[prv] : nullptr;
+            int* lc = LABELS ? lab[cur] : nullptr;
+            // deferred freeze of the level retired last iteration (ptp.cpp:121-130)
+            for (int p = S.frzb + gtid; p < S.frze; p += gthreads) {
+                const int v = ldcg(queue + p);
+                dcur[v] = ldcg(dp + v);
+                if (LABELS) lc[v] = ldcg(lp + v);
+            }
+            // relax the band [bb, be)   (ptp.cpp:96-110)
+            my_max = T(0);
+            const int bb_ = S.bb, ntask = S.be - S.bb, fe_ = S.fe;
+            const int expb = S.expb, expe = S.expe;
+            const int sw = tid / kW;
+            const int stride = nb * (kBlock / kW);
+            for (int t = lb + nb * sw;; t += stride) {
+                const bool act = t < ntask;
+                if (!__any_sync(kFull, act)) break;
+                const int p = bb_ + t;
+                relax_sub<T, LABELS>(M, ring, ringL, act, p, kk, queue, dp, dcur, lp, lc, fe_,
+                                     p >= expb && p < expe, level, queue, &ctl->tail, eps,
+                                     A.last_change, my_max, calls, degs);
+            }
+            const T bmax = block_max(my_max, red_t);
+            if (tid == 0 && bmax > T(0)) atomicMax(&ctl->slot[kk % 3], Lim<T>::bits(bmax));
+            group_barrier(&ctl->bar, epoch, nb, [&] {
+                const T mr = Lim<T>::from_bits(__ldcg(&ctl->slot[kk % 3]));
+                const bool conv = mr < eps;  // ptp.cpp:114
+                const int ub = bb, ue = S.be;
+                upd += static_cast<unsigned long long>(ue - ub);
+                if (lb == 0 && A.trace != nullptr) {
+                    const int row = kk - A.trace_k0;
+                    if (row >= 0 && row < A.trace_cap) {
+                        TraceRow r;
+                        r.k = kk; r.i = i; r.j = S.j; r.conv = conv ? 1 : 0;
+                        r.updated = ue - ub;
+                        r.max_rel = static_cast<double>(mr);
+                        A.trace[row] = r;
+                    }
+                }
+                int nt = tail;
+                if (bfs_open) {
+                    nt = ldcg(&ctl->tail);
+                    if (nt == tail) {
+                        bfs_open = 0;
+                        rho = kk + 1;
+                    } else {
+                        if (lb == 0) limits[kk + 2] = nt;
+                        limk = tail;
+                    }
+                }
+                if (conv) {
+                    frzb = bb;
+                    frze = fe;
+                    bb = fe;
+                    fe = (i + 2 <= kk + 1) ? pf : nt;
+                    ++i;
+                } else {
+                    frzb = frze = 0;
+                }
+                tail = nt;
+                parity ^= 1;
+                k = kk;
+                done = !bfs_open && i > rho - 1;
+            });
+            ++iters;
+        }
+
+        // per-query statistics
+        const long long bc = block_sum(calls, red_l);
+        const long long bd = block_sum(degs, red_l);
+        if (tid == 0) {
+            if (bc) atomicAdd(&ctl->relax, static_cast<unsigned long long>(bc));
+            if (bd) atomicAdd(&ctl->degen, static_cast<unsigned long long>(bd));
+            if (lb == 0) {
+                ctl->k = k; ctl->i = i; ctl->rho = rho; ctl->parity = parity;
+                ctl->bfs_open = bfs_open; ctl->done = done;
+                ctl->s_tail = tail; ctl->s_limk = limk; ctl->s_bb = bb; ctl->s_fe = fe;
+                ctl->s_frzb = frzb; ctl->s_frze = frze;
+                ctl->updates += upd;
+            }
+            S.done = done;
+            S.parity = parity;
+        }
+        __syncthreads();
+        const int fin_done = S.done;
+        const int fin = S.parity;  // buffer written last (ptp.cpp:142)
+        if (!fin_done) continue;   // resumable launch ended mid-run
+
+        // copy-out to original vertex order, widened (ptp.cpp:139-147)
+        double vmax = -1.0;
+        int vidx = INT_MAX;
+        if (A.out_dist != nullptr || A.fps_mode) {
+            const T* df = dist[fin];
+            const int* lf = LABELS ? lab[fin] : nullptr;
+            const long long qo = static_cast<long long>(q) * n;
+            for (int v = gtid; v < n; v += gthreads) {
+                const T x = ldcg(df + v);
+                if (A.out_dist != nullptr) {
+                    if (A.out_double)
+                        static_cast<double*>(A.out_dist)[qo + v] = static_cast<double>(x);
+                    else
+                        static_cast<float*>(A.out_dist)[qo + v] = static_cast<float>(x);
+                }
+                if (A.out_labels != nullptr)
+                    A.out_labels[qo + v] = LABELS ? ldcg(lf + v) : (x != inf ? 0 : -1);
+                const double xd = static_cast<double>(x);
+                if (xd > vmax || (xd == vmax && v < vidx)) {
+                    vmax = xd;
+                    vidx = v;
+                }
+            }
+        }
+        if (A.fps_mode) {
+            // block argmax: max value, lowest index (sampling.cpp:29-36)
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(kFull, vmax, o);
+                const int oi = __shfl_xor_sync(kFull, vidx, o);
+                if (ov > vmax || (ov == vmax && oi < vidx)) { vmax = ov; vidx = oi; }
+            }
+            if ((tid & 31) == 0) { red_v[tid >> 5] = vmax; red_i[tid >> 5] = vidx; }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < kBlock / 32; ++w)
+                    if (red_v[w] > vmax || (red_v[w] == vmax && red_i[w] < vidx)) {
+                        vmax = red_v[w];
+                        vidx = red_i[w];
+                    }
+                A.fps_scratch[2 * blockIdx.x] =
+                    static_cast<unsigned long long>(__double_as_longlong(vmax));
+                A.fps_scratch[2 * blockIdx.x + 1] = static_cast<unsigned long long>(vidx);
+            }
+        }
+        group_barrier(&ctl->bar, epoch, nb, [&] {
+            if (lb != 0) return;
+            QueryStats st;
+            st.relax = static_cast<long long>(__ldcg(&ctl->relax));
+            st.degen = static_cast<long long>(__ldcg(&ctl->degen));
+            st.updates = static_cast<long long>(ctl->updates);
+            st.iterations = k;
+            st.rho = rho;
+            st.unreached = n - tail;
+            st.done = 1;
+            st.radius = 0.0;
+            st.argmax = -1;
+            st.pad = 0;
+            if (A.fps_mode) {
+                double bv = -1.0;
+                int bi = INT_MAX;
+                for (int b = g * nb; b < g * nb + nb; ++b) {
+                    const double ov = __longlong_as_double(
+                        static_cast<long long>(__ldcg(&A.fps_scratch[2 * b])));
+                    const int oi = static_cast<int>(__ldcg(&A.fps_scratch[2 * b + 1]));
+                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                st.radius = bv;
+                st.argmax = bi;
+                if (!A.fps_final) {
+                    if (ldcg(level + bi) == 0) ctl->err = 1;  // would repeat a sample
+                    A.fps_samples[A.src_count] = bi;
+                }
+            }
+            A.qstats[q] = st;
+        });
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void planar_test_kernel(const double* x1, const double* x2, const double* t1,
+                                   const double* t2, int count, double* value, int* side,
+                                   int* degen) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= count) return;
+    const T ax = to_t<T>(x1[3 * q]), ay = to_t<T>(x1[3 * q + 1]), az = to_t<T>(x1[3 * q + 2]);
+    const T bx = to_t<T>(x2[3 * q]), by = to_t<T>(x2[3 * q + 1]), bz = to_t<T>(x2[3 * q + 2]);
+    const T g11 = dot3(ax, ay, az, ax, ay, az), g22 = dot3(bx, by, bz, bx, by, bz);
+    const T g12 = dot3(ax, ay, az, bx, by, bz);
+    T q11, q12, q22, a;
+    const bool dg = corner_geometry(g11, g22, g12, q11, q12, q22, a);
+    int s, d;
+    const T v = corner_candidate(to_t<T>(t1[q]), to_t<T>(t2[q]), sq(g11), sq(g22), q11, q12, q22,
+                                 a, dg, false, s, d);
+    value[q] = static_cast<double>(v);
+    side[q] = s;
+    degen[q] = d;
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+template <typename T>
+void launch_pack(const double* xyz, int n, const int* cptr, const int* ring_in, int* ring_out,
+                 void* ringL, void* quad, cudaStream_t st) {
+    const int blk = 256;
+    pack_kernel<T><<<(n + blk - 1) / blk, blk, 0, st>>>(xyz, n, cptr, ring_in, ring_out,
+                                                        static_cast<T*>(ringL), quad);
+    note_launch();
+}
+template void launch_pack<float>(const double*, int, const int*, const int*, int*, void*, void*,
+                                 cudaStream_t);
+template void launch_pack<double>(const double*, int, const int*, const int*, int*, void*, void*,
+                                  cudaStream_t);
+
+void launch_planar_test(int precision, const double* x1, const double* x2, const double* t1,
+                        const double* t2, int count, double* value, int* side, int* degen,
+                        cudaStream_t st) {
+    const int blk = 128;
+    const int grid = (count + blk - 1) / blk;
+    if (precision == 0)
+        planar_test_kernel<float><<<grid, blk, 0, st>>>(x1, x2, t1, t2, count, value, side, degen);
+    else
+        planar_test_kernel<double><<<grid, blk, 0, st>>>(x1, x2, t1, t2, count, value, side, degen);
+    note_launch();
+}
+
+__global__ void reset_bars_kernel(GroupCtl* ctl, int groups) {
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) ctl[g].bar = 0u;
+}
+
+static const void* run_kernel_ptr(int precision, bool labels) {
+    if (precision == 0)
+        return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<float, true>)
+                      : reinterpret_cast<const void*>(&ptp_run_kernel<float, false>);
+    return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<double, true>)
+                  : reinterpret_cast<const void*>(&ptp_run_kernel<double, false>);
+}
+
+int run_max_blocks(int precision, bool labels, int device) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run_kernel_ptr(precision, labels),
+                                                  kBlock, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return per_sm * sms;
+}
+
+cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st) {
+    const int grid = args.groups * args.blocks_per_group;
+    void* params[] = {const_cast<RunArgs*>(&args)};
+    reset_bars_kernel<<<1, 32, 0, st>>>(args.ctl, args.groups);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = cudaLaunchCooperativeKernel(run_kernel_ptr(precision, labels), dim3(grid), dim3(kBlock),
+                                    params, 0, st);
+    note_launch();
+    return e;
+}
+
+}  // namespace gdb

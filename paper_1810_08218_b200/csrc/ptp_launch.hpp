@@ -1,0 +1,50 @@
+// Host-side launch interface of the device kernels (ptp_kernels.cu, toplesets.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ptp_device.cuh"
+
+namespace gdb {
+
+void note_launch();  // evidence counter (capi.cu)
+
+template <typename T>
+void launch_pack(const double* xyz, int n, const int* cptr, const int* ring_in, int* ring_out,
+                 void* ringL, void* quad, cudaStream_t st);
+
+void launch_planar_test(int precision, const double* x1, const double* x2, const double* t1,
+                        const double* t2, int count, double* value, int* side, int* degen,
+                        cudaStream_t st);
+
+// Max co-resident CTAs of the run kernel on `device` (cooperative launch bound).
+int run_max_blocks(int precision, bool labels, int device);
+cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st);
+
+// Toplesets with the reference's exact ordering (toplesets.cu).
+struct TopoArgs {
+    const int* cptr;
+    const int* ring;  // unflagged ring
+    int n;
+    const int* src;   // m sorted sources
+    int m;
+    int* level;       // n scratch
+    int* queue;       // n: BFS order, then sorted in place per level
+    int* limits;      // n+2
+    int* sorted;      // n (output: exact reference order)
+    int* position;    // n (output)
+    GroupCtl* ctl;
+    int* rho_out;     // device scalar
+    int blocks;
+};
+int topo_max_blocks(int device);
+cudaError_t launch_toplesets(const TopoArgs& a, int* scratch, size_t scratch_words, int* rho_host,
+                             cudaStream_t st);
+
+// reorder_for_bands: old_of_new / new_of_old / permuted faces (toplesets.cu).
+cudaError_t launch_reorder(const int* position, const int* sorted, int reachable, int n,
+                           const int* faces, int nf, int* old_of_new, int* new_of_old,
+                           int* faces_out, cudaStream_t st);
+
+}  // namespace gdb

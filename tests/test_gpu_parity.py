@@ -1,0 +1,214 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the
+reference's golden vectors (bit-exact distances in both precisions, labels,
+K, relax/degenerate counts, band trace, last_change, orderings, FPS), and
+against the C restatement on larger synthetic meshes."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import FPS_CASES, PTP_CASES, bits, golden
+
+import paper_1810_08218_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+
+def mesh_of(gd):
+    return g.Mesh(gd["vertices"], gd["faces"])
+
+
+def test_planar_update_bit_exact():
+    gd = golden("planar_update")
+    for p, prec in (("s", "single"), ("d", "double")):
+        v, s, d = g.planar_update(gd["x1"], gd["x2"], gd["t1"], gd["t2"], precision=prec)
+        assert np.array_equal(bits(v), bits(gd[f"value_{p}"]))
+        assert np.array_equal(s, gd[f"side_{p}"])
+        assert np.array_equal(d, gd[f"degen_{p}"])
+
+
+@pytest.mark.parametrize("name", PTP_CASES)
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_geodesics_bit_exact(name, prec):
+    gd = golden(name)
+    M = mesh_of(gd)
+    p = prec[0]
+    labels = f"labels_{p}" in gd
+    r = g.geodesics(M, gd["sources"], precision=prec, labels=labels, trace=True)
+    assert np.array_equal(bits(r["distances"]), bits(gd[f"dist_{p}"]))
+    assert r["iterations"] == int(gd[f"K_{p}"])
+    assert r["relax_calls"] == int(gd[f"relax_{p}"])
+    assert r["degenerate_calls"] == int(gd[f"degen_{p}"])
+    assert r["unreached"] == int(gd["unreached"])
+    assert r["rho"] == int(gd["rho"])
+    kiju = np.array([[t["k"], t["i"], t["j"], t["updated"]] for t in r["trace"]]).reshape(-1, 4)
+    assert np.array_equal(kiju, gd[f"trace_kijU_{p}"])
+    assert np.array_equal(bits([t["max_rel_change"] for t in r["trace"]]),
+                          bits(gd[f"trace_maxrel_{p}"]))
+    assert [t["front_converged"] for t in r["trace"]] == list(gd[f"trace_conv_{p}"])
+    assert np.array_equal(r["last_change"], gd[f"last_change_{p}"])
+    assert r["vertex_updates"] == int(gd[f"trace_kijU_{p}"][:, 3].sum())
+    if labels:
+        assert np.array_equal(r["labels"], gd[f"labels_{p}"])
+    # without trace the fused fast path must give the same bits
+    r2 = g.geodesics(M, gd["sources"], precision=prec, labels=labels)
+    assert np.array_equal(bits(r2["distances"]), bits(gd[f"dist_{p}"]))
+
+
+@pytest.mark.parametrize("name", PTP_CASES)
+def test_toplesets_exact(name):
+    gd = golden(name)
+    t = g.toplesets(mesh_of(gd), gd["sources"])
+    assert np.array_equal(t["sorted"], gd["sorted"])
+    assert np.array_equal(t["limits"], gd["limits"])
+    assert np.array_equal(t["position"], gd["position"])
+    assert t["rho"] == int(gd["rho"]) and t["unreached"] == int(gd["unreached"])
+
+
+@pytest.mark.parametrize("name", PTP_CASES)
+def test_reorder_for_bands_exact(name):
+    gd = golden(name)
+    M = mesh_of(gd)
+    P, oon, noo = g.reorder_for_bands(M, gd["sources"])
+    assert np.array_equal(oon, gd["old_of_new"])
+    assert np.array_equal(noo, gd["new_of_old"])
+    assert np.array_equal(P.faces(), gd["reordered_faces"])
+    # test_ptp.cpp:159-180: results bit-identical after un-permutation
+    labels = "labels_d" in gd
+    src = noo[gd["sources"]]
+    r = g.geodesics(P, src, labels=labels)
+    assert np.array_equal(bits(r["distances"][noo]), bits(gd["dist_d"]))
+    if labels:
+        assert np.array_equal(r["labels"][noo], gd["labels_d"])
+
+
+@pytest.mark.parametrize("name", PTP_CASES)
+def test_ptp_with_caller_ordering(name):
+    gd = golden(name)
+    M = mesh_of(gd)
+    o = {"sorted": gd["sorted"], "limits": gd["limits"], "position": gd["position"]}
+    labels = "labels_d" in gd
+    for p, prec in (("s", "single"), ("d", "double")):
+        r = g.geodesics_ordered(M, gd["sources"], o, precision=prec, labels=labels)
+        assert np.array_equal(bits(r["distances"]), bits(gd[f"dist_{p}"]))
+        assert r["iterations"] == int(gd[f"K_{p}"])
+
+
+@pytest.mark.parametrize("name", FPS_CASES)
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_fps_and_voronoi_exact(name, prec):
+    gd = golden(name)
+    M = mesh_of(gd)
+    p = prec[0]
+    r = g.farthest_point_sampling(M, int(gd["m"]), seed=int(gd["seed"]), precision=prec)
+    assert np.array_equal(r["samples"], gd[f"samples_{p}"])
+    assert np.array_equal(r["labels"], gd[f"labels_{p}"])
+    assert r["radius"] == float(gd[f"radius_{p}"])
+    assert [h["rho"] for h in r["history"]] == list(gd[f"hist_rho_{p}"])
+    assert [h["relax_calls"] for h in r["history"]] == list(gd[f"hist_relax_{p}"])
+    assert np.array_equal(bits([h["radius"] for h in r["history"]]), bits(gd[f"hist_radius_{p}"]))
+    assert [h["picked"] for h in r["history"]] == list(gd[f"hist_picked_{p}"])
+    lab = g.voronoi(M, gd[f"samples_{p}"], precision=prec)
+    assert np.array_equal(lab, gd[f"voronoi_{p}"])
+
+
+SYNTH = [
+    ("ico5", lambda: g.icosphere_arrays(5), [[0], [5, 700, 9000]]),
+    ("noisy_ico6", lambda: g.noisy_icosphere_arrays(6, 2e-3, 1), [[0], [1, 20000, 33333, 40000]]),
+    ("torus64x48", lambda: g.torus_arrays(64, 48), [[0], [17, 1500, 3000]]),
+    ("height96", lambda: g.heightfield_arrays(96, 96, 20.0, 9.7, 13.1), [[0], [100, 5000, 9000]]),
+    ("grid40_shear2", lambda: g.grid_arrays(40, 40, 2.0), [[820], [0, 1599]]),
+]
+
+
+@pytest.mark.parametrize("name,make,sources", SYNTH, ids=[s[0] for s in SYNTH])
+def test_synthetic_vs_restatement(port_lib, name, make, sources):
+    v, f = make()
+    M = g.Mesh(v, f)
+    P = port_lib.PortMesh(v, f)
+    for src in sources:
+        for prec in ("single", "double"):
+            want = P.ptp(src, precision=prec, labels=True)
+            got = g.geodesics(M, src, precision=prec, labels=True)
+            assert np.array_equal(bits(got["distances"]), bits(want["distances"])), (src, prec)
+            assert np.array_equal(got["labels"], want["labels"])
+            assert got["iterations"] == want["iterations"]
+            assert got["relax_calls"] == want["relax_calls"]
+            assert got["degenerate_calls"] == want["degenerate_calls"]
+
+
+def test_batch_equals_single_runs():
+    v, f = g.noisy_icosphere_arrays(5, 2e-3, 1)
+    M = g.Mesh(v, f)
+    queries = [[q * 97] for q in range(9)] + [[3, 5000, 9000]]
+    for prec in ("single", "double"):
+        for groups in (1, 3, 4):
+            out = g.batch_geodesics(M, queries, precision=prec, labels=True, groups=groups)
+            for q, src in enumerate(queries):
+                one = g.geodesics(M, src, precision=prec, labels=True)
+                assert np.array_equal(bits(out["distances"][q]), bits(one["distances"]))
+                assert np.array_equal(out["labels"][q], one["labels"])
+                assert out["stats"][q]["iterations"] == one["iterations"]
+                assert out["stats"][q]["relax_calls"] == one["relax_calls"]
+
+
+def test_observer_monotone():
+    # test_ptp.cpp:60-74: distances never increase across iterations
+    M = g.generate_grid(9, 9, 2.0)
+    prev = np.full(81, np.inf)
+    ks = []
+
+    def obs(k, d):
+        nonlocal prev
+        assert np.all(d <= prev)
+        prev = d
+        ks.append(k)
+
+    r = g.geodesics(M, [40], observer=obs)
+    assert ks == list(range(1, r["iterations"] + 1))
+    assert np.array_equal(prev, r["distances"])
+
+
+def test_errors_match_reference():
+    M = g.generate_grid(5, 5)
+    with pytest.raises(ValueError, match="empty source set"):
+        g.geodesics(M, [])
+    with pytest.raises(ValueError, match="out of range"):
+        g.geodesics(M, [25])
+    with pytest.raises(ValueError, match="duplicate source"):
+        g.geodesics(M, [3, 3])
+    with pytest.raises(ValueError, match="epsilon must be positive"):
+        g.geodesics(M, [0], epsilon=0.0)
+    with pytest.raises(ValueError, match="precision"):
+        g.geodesics(M, [0], precision="half")
+    with pytest.raises(ValueError, match="sample count"):
+        g.farthest_point_sampling(M, 0)
+    with pytest.raises(ValueError, match="seed"):
+        g.farthest_point_sampling(M, 2, seed=99)
+    with pytest.raises(ValueError, match="empty sample"):
+        g.voronoi(M, [])
+    o = g.toplesets(M, [0])
+    with pytest.raises(ValueError, match="does not match the source set"):
+        g.geodesics_ordered(M, [1], o)
+
+
+def test_reference_properties():
+    # test_ptp.cpp:44-58 sandwich, :182-199 labels, :243-265 K/rho regime
+    for shear in (0.0, 2.0):
+        M = g.generate_grid(9, 7, shear)
+        r = g.geodesics(M, [0])
+        exact = g.grid_reference(M, [0])
+        assert np.all(r["distances"] >= exact * (1 - 1e-12))
+    M = g.generate_grid(9, 5)
+    r = g.geodesics(M, [0, 8], labels=True)
+    assert r["labels"][0] == 0 and r["labels"][8] == 1
+    for j in range(5):
+        assert r["labels"][j * 9 + 1] == 0 and r["labels"][j * 9 + 7] == 1
+    M = g.generate_grid(41, 41)
+    c = 20 * 41 + 20
+    rep = g.mape(g.geodesics(M, [c])["distances"], g.grid_reference(M, [c]), [c])
+    assert rep["mape"] < 3.5
+    S = g.generate_icosphere(3)
+    rep = g.mape(g.geodesics(S, [0])["distances"], g.sphere_reference(S, [0]), [0])
+    assert rep["mape"] < 3.0
