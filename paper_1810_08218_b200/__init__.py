@@ -232,7 +232,7 @@ def _sources(sources):
 
 
 def geodesics(mesh, sources, method="ptp", epsilon=1e-3, precision="double", workers=0,
-              labels=False, trace=False, observer=None):
+              labels=False, trace=False, observer=None, out=None):
     """Distance map from a source set (bindings.cpp:134-175).
 
     Returns ``{"distances", "unreached", ["labels"], "iterations", "relax_calls",
@@ -249,7 +249,9 @@ def geodesics(mesh, sources, method="ptp", epsilon=1e-3, precision="double", wor
     cfg = _config(epsilon, precision, workers, labels, trace)
     src = _sources(sources)
     n = mesh.n_vertices
-    dist = np.empty(n, np.float64)
+    dist = np.empty(n, np.float64) if out is None else out
+    if dist.dtype != np.float64 or dist.shape != (n,) or not dist.flags.c_contiguous:
+        raise ValueError("out must be a contiguous float64 array of n_vertices")
     lab = np.empty(n, np.int32) if labels else None
     stats = _capi.PtpStats()
     cap = 0
@@ -380,6 +382,28 @@ def batch_geodesics(mesh, queries, epsilon=1e-3, precision="single", labels=Fals
     if labels:
         out["labels"] = lab
     return out
+
+
+def batch_geodesics_device(mesh, queries, out_dist_ptr, epsilon=1e-3, precision="single",
+                           out_labels_ptr=None, groups=0, stream=0):
+    """Independent queries with results left in device memory (``out_dist_ptr``:
+    nq*n elements of the run precision, e.g. a torch tensor's data_ptr()).
+    Returns per-query stats; ``device_seconds`` is the CUDA-event time of the launch."""
+    qs = [np.asarray(q, np.int64).reshape(-1) for q in queries]
+    off = np.zeros(len(qs) + 1, np.int32)
+    off[1:] = np.cumsum([len(q) for q in qs])
+    src = np.ascontiguousarray(np.concatenate(qs).astype(np.int32))
+    cfg = _config(epsilon, precision, 0, out_labels_ptr is not None)
+    stats = (_capi.PtpStats * max(len(qs), 1))()
+    check(lib().geodist_batch_device(mesh.handle, src, off, len(qs), C.byref(cfg),
+                                     C.c_void_p(int(out_dist_ptr)),
+                                     C.c_void_p(int(out_labels_ptr)) if out_labels_ptr else None,
+                                     C.cast(stats, C.c_void_p), int(groups),
+                                     C.c_void_p(int(stream)) if stream else None))
+    return [{"iterations": stats[q].iterations, "rho": stats[q].rho,
+             "relax_calls": int(stats[q].relax_calls),
+             "vertex_updates": int(stats[q].vertex_updates), "unreached": stats[q].unreached,
+             "device_seconds": float(stats[q].wall_seconds)} for q in range(len(qs))]
 
 
 def planar_update(x1, x2, t1, t2, precision="double"):

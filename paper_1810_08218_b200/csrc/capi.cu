@@ -10,6 +10,8 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -150,6 +152,9 @@ struct PrecTables {
     int* ring = nullptr;   // ring with degenerate flags for this precision
     void* ringL = nullptr;
     void* quad = nullptr;
+    int* ering = nullptr;  // ELL-8 copies (interleaved)
+    void* eL = nullptr;
+    void* equad = nullptr;
 };
 
 struct geodist_mesh_s {
@@ -174,6 +179,18 @@ struct geodist_mesh_s {
     size_t d_src_cap = 0;
     int* d_i32 = nullptr;  // generic n-sized int buffer
     std::mutex mu;
+    // grow-only per-call device buffers (no cudaMalloc on the solve path)
+    void* pool[8] = {};
+    size_t pool_cap[8] = {};
+    void* buf(int slot, size_t bytes) {
+        if (bytes > pool_cap[slot]) {
+            if (pool[slot]) cudaFree(pool[slot]);
+            pool[slot] = nullptr;
+            pool[slot] = dalloc<char>(bytes);
+            pool_cap[slot] = bytes;
+        }
+        return pool[slot];
+    }
 
     ~geodist_mesh_s() {
         cudaSetDevice(device);
@@ -186,8 +203,11 @@ struct geodist_mesh_s {
                         static_cast<void*>(d_i32)})
             if (p) cudaFree(p);
         for (auto& t : prec)
-            for (void* p : {static_cast<void*>(t.ring), t.ringL, t.quad})
+            for (void* p : {static_cast<void*>(t.ring), t.ringL, t.quad,
+                            static_cast<void*>(t.ering), t.eL, t.equad})
                 if (p) cudaFree(p);
+        for (void* p : pool)
+            if (p) cudaFree(p);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
@@ -201,10 +221,16 @@ struct geodist_mesh_s {
         t.ring = dalloc<int>(ring_len);
         t.ringL = dalloc<char>(ring_len * tsz);
         t.quad = dalloc<char>(static_cast<size_t>(corners > 0 ? corners : 1) * 4 * tsz);
+        const size_t ell = static_cast<size_t>(n > 0 ? n : 1) * kEllW;
+        t.ering = dalloc<int>(ell);
+        t.eL = dalloc<char>(ell * tsz);
+        t.equad = dalloc<char>(ell * 4 * tsz);
         if (p == 0)
-            launch_pack<float>(xyz, n, cptr, ring, t.ring, t.ringL, t.quad, stream);
+            launch_pack<float>(xyz, n, cptr, ring, t.ring, t.ringL, t.quad, t.ering, t.eL, t.equad,
+                               stream);
         else
-            launch_pack<double>(xyz, n, cptr, ring, t.ring, t.ringL, t.quad, stream);
+            launch_pack<double>(xyz, n, cptr, ring, t.ring, t.ringL, t.quad, t.ering, t.eL,
+                                t.equad, stream);
         cuda_ok(cudaGetLastError(), "pack_kernel");
         cuda_ok(cudaStreamSynchronize(stream), "pack_kernel");
     }
@@ -297,18 +323,22 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
     const bool stepwise = q.observer != nullptr && prec == GEODIST_DOUBLE;
     const int chunk = stepwise ? 1 : (want_trace ? 4096 : 0);
 
-    std::unique_ptr<void, DFree> out_buf(dalloc<double>(n));
-    double* d_out = static_cast<double*>(out_buf.get());
-    std::unique_ptr<void, DFree> lab_buf(q.labels ? dalloc<int>(n) : nullptr);
-    std::unique_ptr<void, DFree> lc_buf(want_trace && q.last_change ? dalloc<int>(n) : nullptr);
-    std::unique_ptr<void, DFree> tr_buf(want_trace ? dalloc<TraceRow>(chunk) : nullptr);
-    std::unique_ptr<void, DFree> qs_buf(dalloc<QueryStats>(1));
+    double* d_out = static_cast<double*>(mh->buf(0, sizeof(double) * n));
+    int* d_lab = q.labels ? static_cast<int*>(mh->buf(1, sizeof(int) * n)) : nullptr;
+    int* d_lc = want_trace && q.last_change ? static_cast<int*>(mh->buf(2, sizeof(int) * n))
+                                            : nullptr;
+    TraceRow* d_tr = want_trace ? static_cast<TraceRow*>(mh->buf(3, sizeof(TraceRow) * chunk))
+                                : nullptr;
+    QueryStats* d_qs = static_cast<QueryStats*>(mh->buf(4, sizeof(QueryStats)));
 
     RunArgs a{};
     a.mesh.cptr = mh->cptr;
     a.mesh.ring = mh->prec[prec].ring;
     a.mesh.ringL = mh->prec[prec].ringL;
     a.mesh.quad = mh->prec[prec].quad;
+    a.mesh.ering = mh->prec[prec].ering;
+    a.mesh.eL = mh->prec[prec].eL;
+    a.mesh.equad = mh->prec[prec].equad;
     a.mesh.n = n;
     a.dist0 = ws.dist0;
     a.dist1 = ws.dist1;
@@ -329,15 +359,22 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
     a.fused_bfs = q.ordered ? 0 : 1;
     a.given_rho = q.rho;
     a.max_iters = chunk;
-    a.trace = static_cast<TraceRow*>(tr_buf.get());
+    a.trace = d_tr;
     a.trace_cap = chunk;
-    a.last_change = static_cast<int*>(lc_buf.get());
+    a.last_change = d_lc;
     a.out_dist = d_out;
     a.out_double = 1;
-    a.out_labels = static_cast<int*>(lab_buf.get());
-    a.qstats = static_cast<QueryStats*>(qs_buf.get());
+    a.out_labels = d_lab;
+    a.qstats = d_qs;
     a.fps_mode = 0;
     a.fps_scratch = ws.scratch;
+    if (const char* e = getenv("GEODIST_DEBUG_TIMING")) {
+        a.dbg_iters = atoi(e);
+        a.dbg = static_cast<unsigned long long*>(
+            mh->buf(5, sizeof(unsigned long long) * 3 * static_cast<size_t>(a.dbg_iters) * maxb));
+        cuda_ok(cudaMemsetAsync(a.dbg, 0, sizeof(unsigned long long) * 3 * a.dbg_iters * maxb, st),
+                "dbg");
+    }
 
     std::vector<TraceRow> rows;
     std::vector<double> snap;
@@ -378,6 +415,16 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
     }
     QueryStats qs{};
     cuda_ok(cudaMemcpy(&qs, a.qstats, sizeof(QueryStats), cudaMemcpyDeviceToHost), "stats");
+    if (a.dbg) {
+        std::vector<unsigned long long> h(3 * static_cast<size_t>(a.dbg_iters) * maxb);
+        cuda_ok(cudaMemcpy(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost), "dbg");
+        if (FILE* f = fopen("gpurun_out/dbg_timing.bin", "wb")) {
+            const int hdr[2] = {a.dbg_iters, maxb};
+            fwrite(hdr, sizeof(int), 2, f);
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
+    }
     if (q.distances)
         cuda_ok(cudaMemcpy(q.distances, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost),
                 "read distances");
@@ -439,6 +486,7 @@ int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int3
         if (n < 0 || nf < 0 || (n > 0 && !xyz) || (nf > 0 && !faces))
             throw Fail(GEODIST_EINVAL, "invalid mesh arrays");
         Fans fans = build_fans(xyz, n, faces, nf);  // runtime_error -> EMESH
+        if (n > kIdMask) throw Fail(GEODIST_EINVAL, "mesh too large: at most 2^27-1 vertices");
         require_device(device);
         std::unique_ptr<geodist_mesh_s> m(new geodist_mesh_s);
         m->device = device;
@@ -735,6 +783,9 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         a.mesh.ring = mh->prec[prec].ring;
         a.mesh.ringL = mh->prec[prec].ringL;
         a.mesh.quad = mh->prec[prec].quad;
+        a.mesh.ering = mh->prec[prec].ering;
+        a.mesh.eL = mh->prec[prec].eL;
+        a.mesh.equad = mh->prec[prec].equad;
         a.mesh.n = n;
         a.dist0 = ws.dist0;
         a.dist1 = ws.dist1;
@@ -833,6 +884,9 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         a.mesh.ring = mh->prec[prec].ring;
         a.mesh.ringL = mh->prec[prec].ringL;
         a.mesh.quad = mh->prec[prec].quad;
+        a.mesh.ering = mh->prec[prec].ering;
+        a.mesh.eL = mh->prec[prec].eL;
+        a.mesh.equad = mh->prec[prec].equad;
         a.mesh.n = n;
         a.dist0 = ws.dist0;
         a.dist1 = ws.dist1;

@@ -24,8 +24,17 @@
 namespace gdb {
 
 constexpr int kBlock = 512;        // threads per CTA
-constexpr int kW = 8;              // lanes per vertex (sub-warp): 7 corners per pass
+constexpr int kW = 8;              // lanes per vertex in the BFS-only kernel
+constexpr int kGroup = 4;          // lanes per vertex in the solver: 2 ring entries per lane
+constexpr int kEllW = 8;           // ELL slot: 8 ring entries (<= 7 corners) per vertex
+constexpr int kMetaShift = 27;     // entry 0 bits 27..30 hold the corner count d
+constexpr int kIdMask = (1 << kMetaShift) - 1;
+constexpr int kEllOverflow = 15;   // d code: more than 7 corners, use the CSR tables
 constexpr unsigned kFull = 0xffffffffu;
+
+// ELL entry e of a vertex lives at slot (e % 4) * 2 + e / 4, so lane l of a
+// 4-lane group reads entries l and l + 4 as one 8-byte (or 16-byte) vector.
+__host__ __device__ constexpr int ell_slot(int e) { return (e & 3) * 2 + (e >> 2); }
 
 // One group of CTAs runs one query; its control block lives in global memory.
 // Hot words sit on separate 128-byte lines.
@@ -59,10 +68,13 @@ struct TraceRow {  // mirrors geodist_band_row
 };
 
 struct MeshDev {
-    const int* cptr;
-    const int* ring;
+    const int* cptr;   // CSR (overflow vertices, BFS seeding)
+    const int* ring;   // CSR ring with degenerate flags for this precision
     const void* ringL;
     const void* quad;
+    const int* ering;  // ELL-8 ring (interleaved, meta in entry 0)
+    const void* eL;    // ELL-8 |x|
+    const void* equad; // ELL-8 Gram inverse quads
     int n;
 };
 
@@ -105,7 +117,17 @@ struct RunArgs {
     unsigned long long* fps_scratch;  // 2 * gridDim.x words
     int* fps_samples;                 // device sample list (== src)
     int fps_final;
+    // optional per-iteration timestamps (globaltimer ns): [iter][cta][3] =
+    // (work start, work end after the CTA reduction, barrier release)
+    unsigned long long* dbg;
+    int dbg_iters;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }

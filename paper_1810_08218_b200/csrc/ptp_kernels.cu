@@ -157,8 +157,27 @@ template <> struct Quad<double> {
     }
 };
 
+template <typename T> struct Ell2;
+template <> struct Ell2<float> {
+    __device__ __forceinline__ static void load(const void* base, size_t at, float& a, float& b) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(static_cast<const float*>(base) + at));
+        a = v.x;
+        b = v.y;
+    }
+};
+template <> struct Ell2<double> {
+    __device__ __forceinline__ static void load(const void* base, size_t at, double& a, double& b) {
+        const double2 v =
+            __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(base) + at));
+        a = v.x;
+        b = v.y;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // one-time geometry pack (per mesh, per precision)
+
+// CSR tables: per-ring |x|, per-corner Gram inverse, degenerate flag in bit 31.
 template <typename T>
 __global__ void pack_kernel(const double* __restrict__ xyz, int n, const int* __restrict__ cptr,
                             const int* __restrict__ ring_in, int* __restrict__ ring_out,
@@ -194,20 +213,59 @@ __global__ void pack_kernel(const double* __restrict__ xyz, int n, const int* __
     }
 }
 
+// ELL-8 tables (kEllW ring entries per vertex, interleaved so that lane l of a
+// 4-lane group reads entries l and l+4 with one vector load).  Vertices with
+// more than kEllW-1 corners are marked overflow and use the CSR tables.
+template <typename T>
+__global__ void pack_ell_kernel(int n, const int* __restrict__ cptr,
+                                const int* __restrict__ ring_f, const T* __restrict__ ringL,
+                                const void* __restrict__ quad, int* __restrict__ ering,
+                                T* __restrict__ eL, void* __restrict__ equad) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int c0 = cptr[v], d = cptr[v + 1] - c0, r0 = c0 + v;
+    const size_t b = static_cast<size_t>(v) * kEllW;
+    if (d > kEllW - 1) {
+        for (int e = 0; e < kEllW; ++e) {
+            ering[b + ell_slot(e)] = e == 0 ? (v | (kEllOverflow << kMetaShift)) : v;
+            eL[b + ell_slot(e)] = T(0);
+            Quad<T>::store(equad, static_cast<int>(b + ell_slot(e)), T(0), T(0), T(0), T(0));
+        }
+        return;
+    }
+    for (int e = 0; e < kEllW; ++e) {
+        const bool has = d > 0 && e <= d;
+        int val = has ? ring_f[r0 + e] : v;  // bit 31: corner e is degenerate
+        if (e == 0) val = (val & (INT_MIN | kIdMask)) | (d << kMetaShift);
+        ering[b + ell_slot(e)] = val;
+        eL[b + ell_slot(e)] = has ? ringL[r0 + e] : T(0);
+        Quad<T> q;
+        if (e < d) {
+            q.load(quad, c0 + e);
+        } else {
+            q.q11 = q.q12 = q.q22 = q.a = T(0);
+        }
+        Quad<T>::store(equad, static_cast<int>(b + ell_slot(e)), q.q11, q.q12, q.q22, q.a);
+    }
+}
+
 // ---------------------------------------------------------------------------
-// group barrier: all CTAs of one group; thread 0 runs `post` after release
+// group barrier (all CTAs of one query): release-add arrival, acquire polling.
+// Thread 0 runs `post` after the release, before the closing __syncthreads.
+__device__ __forceinline__ void red_release(unsigned* p, unsigned x) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+
 template <typename Post>
 __device__ __forceinline__ void group_barrier(unsigned* bar, unsigned& epoch, unsigned nblk,
                                               Post&& post) {
     __syncthreads();
     if (threadIdx.x == 0) {
         ++epoch;
-        __threadfence();
-        atomicAdd(bar, 1u);
+        red_release(bar, 1u);
         const unsigned target = epoch * nblk;
         while (static_cast<int>(ld_acquire(bar) - target) < 0) {
         }
-        __threadfence();
         post();
     }
     __syncthreads();
@@ -229,8 +287,7 @@ __device__ __forceinline__ T block_max(T x, T* red) {
             r = y > r ? y : r;
         }
     }
-    __syncthreads();
-    return r;  // valid in thread 0
+    return r;  // valid in thread 0; caller's barrier orders the next use of `red`
 }
 
 __device__ __forceinline__ long long block_sum(long long x, long long* red) {
@@ -250,95 +307,200 @@ struct Bcast {
     int k, i, j, bb, fe, be, expb, expe, frzb, frze, parity, done;
 };
 
-// Relax one band vertex per sub-warp (all 32 lanes of the warp call this in
-// lock-step; `act` predicates the sub-warp).  Fused BFS: lanes holding ring
-// ids of a level-k vertex claim unvisited neighbours for level k+1.
+// Warp-aggregated append of claimed vertices to the BFS queue.
+__device__ __forceinline__ void append_claims(bool claim, int id, int* tail, int* queue) {
+    const unsigned bal = __ballot_sync(kFull, claim);
+    if (bal) {
+        const int l32 = threadIdx.x & 31;
+        const int leader = __ffs(bal) - 1;
+        int base = 0;
+        if (l32 == leader) base = atomicAdd(tail, __popc(bal));
+        base = __shfl_sync(kFull, base, leader);
+        if (claim) queue[base + __popc(bal & ((1u << l32) - 1u))] = id;
+    }
+}
+
+// Candidates of the corners one lane holds in a chunk.  Lane gl holds ring
+// entries gl and gl+4 of the chunk; corner c = (entry c, entry c+1), so
+//   corner gl   pairs (gl, gl+1): entry gl+1 is lane gl+1's first entry, except
+//                                  for lane 3 where entry 4 is lane 0's second;
+//   corner gl+4 pairs (gl+4, gl+5): entry gl+5 is lane gl+1's second (lanes 0-2).
 template <typename T, bool LABELS>
-__device__ __forceinline__ void relax_sub(const MeshDev& M, const int* __restrict__ ring,
-                                          const T* __restrict__ ringL, bool act, int p, int kk,
-                                          const int* queue, const T* dp, T* dc, const int* lp,
-                                          int* lc, int fe, bool expand, int* level, int* queue_w,
-                                          int* tail_ptr, T eps, int* last_change, T& my_max,
-                                          long long& calls, long long& degs) {
+__device__ __forceinline__ void chunk_candidates(int gl, int cbase, int d, int ra, int rb,
+                                                 T La, T Lb, T ta, T tb, int la, int lb_,
+                                                 const Quad<T>& qa, const Quad<T>& qb,
+                                                 T& best, int& bidx, int& blab, long long& degs) {
     const T inf = Lim<T>::inf();
-    const int lane = threadIdx.x & (kW - 1);
-    int v = 0, c0 = 0, d = 0;
-    if (act) {
-        v = ldcg(queue + p);
-        c0 = __ldg(M.cptr + v);
-        d = __ldg(M.cptr + v + 1) - c0;
+    const int nx = (gl + 1) & (kGroup - 1);
+    const T ta_r = __shfl_sync(kFull, ta, nx, kGroup);
+    const T tb_r = __shfl_sync(kFull, tb, nx, kGroup);
+    const T La_r = __shfl_sync(kFull, La, nx, kGroup);
+    const T Lb_r = __shfl_sync(kFull, Lb, nx, kGroup);
+    int la_r = -1, lb_r = -1;
+    if (LABELS) {
+        la_r = __shfl_sync(kFull, la, nx, kGroup);
+        lb_r = __shfl_sync(kFull, lb_, nx, kGroup);
     }
-    const int r0 = c0 + v;
-    const T tv = act ? ldcg(dp + v) : inf;
+    const bool last = gl == kGroup - 1;
+    const int ca = cbase + gl;
+    if (ca < d) {
+        const T t2 = last ? tb_r : ta_r;
+        const T L2 = last ? Lb_r : La_r;
+        const int l2 = last ? lb_r : la_r;
+        const bool mixed = LABELS && la != l2 && ta != inf && t2 != inf;
+        int side, deg;
+        const T val = corner_candidate(ta, t2, La, L2, qa.q11, qa.q12, qa.q22, qa.a, ra < 0, mixed,
+                                       side, deg);
+        degs += deg;
+        if (val < best) {
+            best = val;
+            bidx = ca;
+            if (LABELS) blab = side == 0 ? la : l2;
+        }
+    }
+    const int cb = ca + kGroup;
+    if (!last && cb < d) {
+        const bool mixed = LABELS && lb_ != lb_r && tb != inf && tb_r != inf;
+        int side, deg;
+        const T val = corner_candidate(tb, tb_r, Lb, Lb_r, qb.q11, qb.q12, qb.q22, qb.a, rb < 0,
+                                       mixed, side, deg);
+        degs += deg;
+        if (val < best) {
+            best = val;
+            bidx = cb;
+            if (LABELS) blab = side == 0 ? lb_ : lb_r;
+        }
+    }
+}
+
+// Relax one band vertex per 4-lane group (relax_vertex, update_kernel.hpp:93-120).
+// All 32 lanes call this in lock-step; `act` predicates the group.  Lanes
+// holding ring ids of a level-k vertex also claim unvisited neighbours for
+// level k+1 (toplesets.cpp:44-52), issued right after the ring ids arrive.
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax_group(const MeshDev& M, bool act, int p, int kk,
+                                            const int* queue, const T* dp, T* dc, const int* lp,
+                                            int* lc, int fe, bool expand, int* level,
+                                            int* queue_w, int* tail_ptr, T eps, int* last_change,
+                                            T& my_max, long long& calls, long long& degs) {
+    const T inf = Lim<T>::inf();
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int g0 = (threadIdx.x & 31) & ~(kGroup - 1);  // group's lane 0 within the warp
+    int v = 0;
+    if (act) v = ldcg(queue + p);
+    const size_t eb = static_cast<size_t>(v) * kEllW;
+    // ELL fast path: entries gl and gl+4, corners gl and gl+4 (one vector load each)
+    int2 rr = make_int2(0, 0);
+    T La = T(0), Lb = T(0);
+    Quad<T> qa, qb;
+    T tv = inf;
     int lv = -1;
-    if (LABELS && act) lv = ldcg(lp + v);
-    int nch = d > 0 ? (d + kW - 2) / (kW - 1) : 0;
-    nch = __reduce_max_sync(kFull, nch);
-    T best = lane == 0 ? tv : inf;
-    int bidx = lane == 0 ? -1 : INT_MAX;
-    int blab = lane == 0 ? lv : -1;
-    const bool exp = act && expand;
-    for (int ch = 0; ch < nch; ++ch) {
-        const int e = ch * (kW - 1) + lane;  // ring entry == corner index
-        const bool has = act && d > 0 && e <= d;
-        int rid = 0;
-        T L = T(0), t = inf;
-        int l = -1;
-        if (has) {
-            rid = __ldg(ring + r0 + e);
-            L = __ldg(ringL + r0 + e);
+    if (act) {
+        rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
+        Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
+        qa.load(M.equad, static_cast<int>(eb + 2 * gl));
+        qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
+        tv = ldcg(dp + v);
+        if (LABELS) lv = ldcg(lp + v);
+    }
+    const int meta = __shfl_sync(kFull, rr.x, g0);
+    int d = act ? (meta >> kMetaShift) & 15 : 0;
+    const bool ovf = d == kEllOverflow;
+    const int ida = rr.x & kIdMask, idb = rr.y & kIdMask;
+    const bool hasa = act && !ovf && d > 0 && gl <= d;
+    const bool hasb = act && !ovf && d > 0 && gl + kGroup <= d;
+    // BFS claims first: they depend on the ring ids only
+    bool ca_claim = false, cb_claim = false;
+    if (expand) {
+        if (hasa) ca_claim = atomicCAS(level + ida, -1, kk + 1) == -1;
+        if (hasb) cb_claim = atomicCAS(level + idb, -1, kk + 1) == -1;
+    }
+    T ta = inf, tb = inf;
+    int la = -1, lb_ = -1;
+    if (hasa) {
+        ta = ldcg(dp + ida);
+        if (LABELS) la = ldcg(lp + ida);
+    }
+    if (hasb) {
+        tb = ldcg(dp + idb);
+        if (LABELS) lb_ = ldcg(lp + idb);
+    }
+    T best = gl == 0 ? tv : inf;
+    int bidx = gl == 0 ? -1 : INT_MAX;
+    int blab = gl == 0 ? lv : -1;
+    chunk_candidates<T, LABELS>(gl, 0, ovf ? 0 : d, rr.x, rr.y, La, Lb, ta, tb, la, lb_, qa, qb,
+                                best, bidx, blab, degs);
+    append_claims(ca_claim, ida, tail_ptr, queue_w);
+    append_claims(cb_claim, idb, tail_ptr, queue_w);
+
+    // overflow vertices (> 7 corners): CSR tables, 7 corners per chunk
+    if (__any_sync(kFull, act && ovf)) {
+        int c0 = 0;
+        if (act && ovf) {
+            c0 = __ldg(M.cptr + v);
+            d = __ldg(M.cptr + v + 1) - c0;
         }
-        const int id = rid & INT_MAX;
-        if (has) {
-            t = ldcg(dp + id);
-            if (LABELS) l = ldcg(lp + id);
-        }
-        const T t2 = __shfl_down_sync(kFull, t, 1, kW);
-        const T L2 = __shfl_down_sync(kFull, L, 1, kW);
-        int l2 = -1;
-        if (LABELS) l2 = __shfl_down_sync(kFull, l, 1, kW);
-        if (has && lane < kW - 1 && e < d) {
-            Quad<T> q;
-            q.load(M.quad, c0 + e);
-            const bool mixed = LABELS && l != l2 && t != inf && t2 != inf;
-            int side, deg;
-            const T val = corner_candidate(t, t2, L, L2, q.q11, q.q12, q.q22, q.a, rid < 0, mixed,
-                                           side, deg);
-            degs += deg;
-            if (val < best) {
-                best = val;
-                bidx = e;
-                if (LABELS) blab = side == 0 ? l : l2;
+        const int r0 = c0 + v;
+        int nch = act && ovf ? (d + kEllW - 2) / (kEllW - 1) : 0;
+        nch = __reduce_max_sync(kFull, nch);
+        const int* ring = M.ring;
+        const T* ringL = static_cast<const T*>(M.ringL);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int base = ch * (kEllW - 1);
+            const int ea = base + gl, ebb = base + gl + kGroup;
+            const bool ha = act && ovf && ea <= d, hb = act && ovf && ebb <= d;
+            int xa = 0, xb = 0;
+            T LA = T(0), LB = T(0), TA = inf, TB = inf;
+            int lA = -1, lB = -1;
+            Quad<T> QA, QB;
+            QA.q11 = QA.q12 = QA.q22 = QA.a = T(0);
+            QB = QA;
+            if (ha) {
+                xa = __ldg(ring + r0 + ea);
+                LA = __ldg(ringL + r0 + ea);
+                if (ea < d) QA.load(M.quad, c0 + ea);
             }
-        }
-        // fused BFS expansion (toplesets.cpp:44-52)
-        bool claim = false;
-        if (exp && has) {
-            if (ldcg(level + id) < 0) claim = atomicCAS(level + id, -1, kk + 1) == -1;
-        }
-        const unsigned bal = __ballot_sync(kFull, claim);
-        if (bal) {
-            const int l32 = threadIdx.x & 31;
-            const int leader = __ffs(bal) - 1;
-            int base = 0;
-            if (l32 == leader) base = atomicAdd(tail_ptr, __popc(bal));
-            base = __shfl_sync(kFull, base, leader);
-            if (claim) queue_w[base + __popc(bal & ((1u << l32) - 1u))] = id;
+            if (hb) {
+                xb = __ldg(ring + r0 + ebb);
+                LB = __ldg(ringL + r0 + ebb);
+                if (ebb < d) QB.load(M.quad, c0 + ebb);
+            }
+            const int ia = xa & INT_MAX, ib = xb & INT_MAX;
+            bool cA = false, cB = false;
+            if (expand) {
+                if (ha) cA = atomicCAS(level + ia, -1, kk + 1) == -1;
+                if (hb) cB = atomicCAS(level + ib, -1, kk + 1) == -1;
+            }
+            if (ha) {
+                TA = ldcg(dp + ia);
+                if (LABELS) lA = ldcg(lp + ia);
+            }
+            if (hb) {
+                TB = ldcg(dp + ib);
+                if (LABELS) lB = ldcg(lp + ib);
+            }
+            // corners base+gl and base+gl+4 of this chunk; cap at 7 corners per chunk
+            const int dlim = act && ovf ? min(d, base + kEllW - 1) : 0;
+            chunk_candidates<T, LABELS>(gl, base, dlim, xa, xb, LA, LB, TA, TB, lA, lB, QA, QB,
+                                        best, bidx, blab, degs);
+            append_claims(cA, ia, tail_ptr, queue_w);
+            append_claims(cB, ib, tail_ptr, queue_w);
         }
     }
-    // lexicographic (value, corner) min over the sub-warp == first strict-'<' winner
-    for (int o = kW / 2; o > 0; o >>= 1) {
-        const T ob = __shfl_xor_sync(kFull, best, o, kW);
-        const int oi = __shfl_xor_sync(kFull, bidx, o, kW);
+
+    // lexicographic (value, corner) min over the group == first strict-'<' winner
+    for (int o = kGroup / 2; o > 0; o >>= 1) {
+        const T ob = __shfl_xor_sync(kFull, best, o, kGroup);
+        const int oi = __shfl_xor_sync(kFull, bidx, o, kGroup);
         int ol = -1;
-        if (LABELS) ol = __shfl_xor_sync(kFull, blab, o, kW);
+        if (LABELS) ol = __shfl_xor_sync(kFull, blab, o, kGroup);
         if (ob < best || (ob == best && oi < bidx)) {
             best = ob;
             bidx = oi;
             if (LABELS) blab = ol;
         }
     }
-    if (act && lane == 0) {
+    if (act && gl == 0) {
         dc[v] = best;
         if (LABELS) lc[v] = blab;
         calls += d;
@@ -373,13 +535,14 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
     int* limits = A.limits + off;
     const MeshDev M = A.mesh;
     const int n = M.n;
-    const int* ring = M.ring;
-    const T* ringL = static_cast<const T*>(M.ringL);
     const T inf = Lim<T>::inf();
     const T eps = static_cast<T>(A.eps);
     unsigned epoch = 0;
     const int gthreads = nb * kBlock;
     const int gtid = lb * kBlock + tid;
+    constexpr int kGroupsPerBlock = kBlock / kGroup;
+    const int stride = nb * kGroupsPerBlock;
+    const int first_task = lb + nb * (tid / kGroup);
 
     for (int q = g; q < A.nq; q += A.groups) {
         const int s0 = A.src_off ? A.src_off[q] : 0;
@@ -389,6 +552,29 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
         int k = 0, i = 1, rho = INT_MAX, parity = 0, bfs_open = 0, done = 0;
         int tail = 0, limk = 0, bb = 0, fe = 0, frzb = 0, frze = 0;
         unsigned long long upd = 0;
+        int pf = -1;
+        // fills S for the iteration after `k` (thread 0)
+        auto publish = [&] {
+            S.done = done;
+            if (done) return;
+            const int kk = k + 1;
+            const int j = bfs_open ? kk : min(kk, rho - 1);
+            S.k = kk;
+            S.i = i;
+            S.j = j;
+            S.bb = bb;
+            S.fe = fe;
+            S.be = (bfs_open || j + 1 == rho) ? tail : ldcg(limits + j + 1);
+            S.expb = bfs_open ? limk : 0;
+            S.expe = bfs_open ? tail : 0;
+            S.frzb = frzb;
+            S.frze = frze;
+            S.parity = parity;
+            pf = -1;
+            if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
+                pf = (bfs_open && i + 2 == kk + 1) ? tail : ldcg(limits + i + 2);
+            if (lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
+        };
 
         if (A.phase_init) {
             // reset (ptp.cpp:61-68)
@@ -429,45 +615,30 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
             }
             group_barrier(&ctl->bar, epoch, nb, [] {});
             if (A.fused_bfs) {
-                // iteration 0: level 0 -> level 1
-                const int sw = tid / kW;
-                const int stride = nb * (kBlock / kW);
-                T dummy_max = T(0);
-                long long dc0 = 0, dd0 = 0;
-                for (int t = lb + nb * sw;; t += stride) {
+                // iteration 0: level 0 -> level 1 (ring walk only; sources are never relaxed)
+                const int gl = tid & (kGroup - 1);
+                for (int t = first_task;; t += stride) {
                     const bool act = t < m;
                     if (!__any_sync(kFull, act)) break;
-                    // expansion only: relax of a source is skipped (sources are never
-                    // in a band); reuse the sub-warp ring walk with writes disabled
-                    const int lane = tid & (kW - 1);
                     int v = 0, c0 = 0, d = 0;
                     if (act) {
                         v = ldcg(queue + t);
                         c0 = __ldg(M.cptr + v);
                         d = __ldg(M.cptr + v + 1) - c0;
                     }
-                    int nch = d > 0 ? (d + kW) / kW : 0;  // ring entries 0..d
+                    int nch = d > 0 ? (d + kGroup) / kGroup : 0;  // ring entries 0..d
                     nch = __reduce_max_sync(kFull, nch);
                     for (int ch = 0; ch < nch; ++ch) {
-                        const int e = ch * kW + lane;
+                        const int e = ch * kGroup + gl;
                         bool claim = false;
                         int id = 0;
                         if (act && d > 0 && e <= d) {
-                            id = __ldg(ring + c0 + v + e) & INT_MAX;
-                            if (ldcg(level + id) < 0) claim = atomicCAS(level + id, -1, 1) == -1;
+                            id = __ldg(M.ring + c0 + v + e) & INT_MAX;
+                            claim = atomicCAS(level + id, -1, 1) == -1;
                         }
-                        const unsigned bal = __ballot_sync(kFull, claim);
-                        if (bal) {
-                            const int l32 = tid & 31;
-                            const int leader = __ffs(bal) - 1;
-                            int base = 0;
-                            if (l32 == leader) base = atomicAdd(&ctl->tail, __popc(bal));
-                            base = __shfl_sync(kFull, base, leader);
-                            if (claim) queue[base + __popc(bal & ((1u << l32) - 1u))] = id;
-                        }
+                        append_claims(claim, id, &ctl->tail, queue);
                     }
                 }
-                (void)dummy_max; (void)dc0; (void)dd0;
             }
             group_barrier(&ctl->bar, epoch, nb, [&] {
                 if (A.fused_bfs) {
@@ -491,75 +662,62 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
                     fe = rho >= 2 ? ldcg(limits + 2) : tail;
                 }
                 done = !bfs_open && i > rho - 1;
+                publish();
             });
-        } else if (tid == 0) {
-            // resume
-            k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
-            bfs_open = ctl->bfs_open; done = ctl->done;
-            tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
-            frzb = ctl->s_frzb; frze = ctl->s_frze;
+        } else {
+            if (tid == 0) {
+                // resume a run stopped by max_iters
+                k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
+                bfs_open = ctl->bfs_open; done = ctl->done;
+                tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
+                frzb = ctl->s_frzb; frze = ctl->s_frze;
+                publish();
+            }
+            __syncthreads();
         }
 
         T my_max = T(0);
         long long calls = 0, degs = 0;
         int iters = 0;
-        int pf = -1;
         for (;;) {
-            if (tid == 0) {
-                const bool stop = done || (A.max_iters > 0 && iters >= A.max_iters);
-                S.done = stop ? 1 : 0;
-                if (!stop) {
-                    const int kk = k + 1;
-                    const int j = bfs_open ? kk : min(kk, rho - 1);
-                    S.k = kk;
-                    S.i = i;
-                    S.j = j;
-                    S.bb = bb;
-                    S.fe = fe;
-                    S.be = (bfs_open || j + 1 == rho) ? tail : ldcg(limits + j + 1);
-                    S.expb = bfs_open ? limk : 0;
-                    S.expe = bfs_open ? tail : 0;
-                    S.frzb = frzb;
-                    S.frze = frze;
-                    S.parity = parity;
-                    pf = -1;
-                    if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
-                        pf = (bfs_open && i + 2 == kk + 1) ? tail : ldcg(limits + i + 2);
-                    if (lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
-                }
-            }
-            __syncthreads();
-            if (S.done) break;
+            // S was filled by thread 0 inside the previous barrier
+            if (S.done || (A.max_iters > 0 && iters >= A.max_iters)) break;
             const int kk = S.k;
+            const bool dbg = A.dbg != nullptr && tid == 0 && iters < A.dbg_iters;
+            unsigned long long* dslot =
+                dbg ? A.dbg + 3 * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
+            if (dbg) dslot[0] = gtimer();
             const int prv = S.parity, cur = prv ^ 1;
             const T* dp = dist[prv];
             T* dcur = dist[cur];
             const int* lp = LABELS ? lab[prv] : nullptr;
             int* lc = LABELS ? lab[cur] : nullptr;
+            const int bb_ = S.bb, ntask = S.be - S.bb, fe_ = S.fe;
+            const int expb = S.expb, expe = S.expe;
+            const int frzb_ = S.frzb, frze_ = S.frze;
             // deferred freeze of the level retired last iteration (ptp.cpp:121-130)
-            for (int p = S.frzb + gtid; p < S.frze; p += gthreads) {
+            for (int p = frzb_ + gtid; p < frze_; p += gthreads) {
                 const int v = ldcg(queue + p);
                 dcur[v] = ldcg(dp + v);
                 if (LABELS) lc[v] = ldcg(lp + v);
             }
             // relax the band [bb, be)   (ptp.cpp:96-110)
             my_max = T(0);
-            const int bb_ = S.bb, ntask = S.be - S.bb, fe_ = S.fe;
-            const int expb = S.expb, expe = S.expe;
-            const int sw = tid / kW;
-            const int stride = nb * (kBlock / kW);
-            for (int t = lb + nb * sw;; t += stride) {
+            for (int t = first_task;; t += stride) {
                 const bool act = t < ntask;
                 if (!__any_sync(kFull, act)) break;
                 const int p = bb_ + t;
-                relax_sub<T, LABELS>(M, ring, ringL, act, p, kk, queue, dp, dcur, lp, lc, fe_,
-                                     p >= expb && p < expe, level, queue, &ctl->tail, eps,
-                                     A.last_change, my_max, calls, degs);
+                relax_group<T, LABELS>(M, act, p, kk, queue, dp, dcur, lp, lc, fe_,
+                                       p >= expb && p < expe, level, queue, &ctl->tail, eps,
+                                       A.last_change, my_max, calls, degs);
             }
             const T bmax = block_max(my_max, red_t);
+            if (dbg) dslot[1] = gtimer();
             if (tid == 0 && bmax > T(0)) atomicMax(&ctl->slot[kk % 3], Lim<T>::bits(bmax));
             group_barrier(&ctl->bar, epoch, nb, [&] {
+                if (dbg) dslot[2] = gtimer();
                 const T mr = Lim<T>::from_bits(__ldcg(&ctl->slot[kk % 3]));
+                const int nt = bfs_open ? ldcg(&ctl->tail) : tail;
                 const bool conv = mr < eps;  // ptp.cpp:114
                 const int ub = bb, ue = S.be;
                 upd += static_cast<unsigned long long>(ue - ub);
@@ -573,9 +731,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
                         A.trace[row] = r;
                     }
                 }
-                int nt = tail;
                 if (bfs_open) {
-                    nt = ldcg(&ctl->tail);
                     if (nt == tail) {
                         bfs_open = 0;
                         rho = kk + 1;
@@ -597,6 +753,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
                 parity ^= 1;
                 k = kk;
                 done = !bfs_open && i > rho - 1;
+                publish();
             });
             ++iters;
         }
@@ -625,7 +782,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
         // copy-out to original vertex order, widened (ptp.cpp:139-147)
         double vmax = -1.0;
         int vidx = INT_MAX;
-        if (A.out_dist != nullptr || A.fps_mode) {
+        if (A.out_dist != nullptr || A.fps_mode || A.out_labels != nullptr) {
             const T* df = dist[fin];
             const int* lf = LABELS ? lab[fin] : nullptr;
             const long long qo = static_cast<long long>(q) * n;
@@ -726,16 +883,21 @@ __global__ void planar_test_kernel(const double* x1, const double* x2, const dou
 
 template <typename T>
 void launch_pack(const double* xyz, int n, const int* cptr, const int* ring_in, int* ring_out,
-                 void* ringL, void* quad, cudaStream_t st) {
+                 void* ringL, void* quad, int* ering, void* eL, void* equad, cudaStream_t st) {
     const int blk = 256;
-    pack_kernel<T><<<(n + blk - 1) / blk, blk, 0, st>>>(xyz, n, cptr, ring_in, ring_out,
-                                                        static_cast<T*>(ringL), quad);
+    const int grid = (n + blk - 1) / blk;
+    if (grid == 0) return;
+    pack_kernel<T><<<grid, blk, 0, st>>>(xyz, n, cptr, ring_in, ring_out, static_cast<T*>(ringL),
+                                         quad);
+    note_launch();
+    pack_ell_kernel<T><<<grid, blk, 0, st>>>(n, cptr, ring_out, static_cast<const T*>(ringL),
+                                             quad, ering, static_cast<T*>(eL), equad);
     note_launch();
 }
 template void launch_pack<float>(const double*, int, const int*, const int*, int*, void*, void*,
-                                 cudaStream_t);
+                                 int*, void*, void*, cudaStream_t);
 template void launch_pack<double>(const double*, int, const int*, const int*, int*, void*, void*,
-                                  cudaStream_t);
+                                  int*, void*, void*, cudaStream_t);
 
 void launch_planar_test(int precision, const double* x1, const double* x2, const double* t1,
                         const double* t2, int count, double* value, int* side, int* degen,

@@ -12,7 +12,7 @@ void note_launch();  // evidence counter (capi.cu)
 
 template <typename T>
 void launch_pack(const double* xyz, int n, const int* cptr, const int* ring_in, int* ring_out,
-                 void* ringL, void* quad, cudaStream_t st);
+                 void* ringL, void* quad, int* ering, void* eL, void* equad, cudaStream_t st);
 
 void launch_planar_test(int precision, const double* x1, const double* x2, const double* t1,
                         const double* t2, int count, double* value, int* side, int* degen,

@@ -1,0 +1,23 @@
+import numpy as np, sys
+raw = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/dbg_timing.bin", "rb").read()
+it, nb = np.frombuffer(raw[:8], np.int32)
+t = np.frombuffer(raw[8:], np.uint64).reshape(it, nb, 3).astype(np.int64)
+valid = (t[:, :, 0] > 0).all(axis=1)
+t = t[valid]
+base = t[:, :, 0].min(axis=1, keepdims=True)
+start = t[:, :, 0] - base
+work = t[:, :, 1] - t[:, :, 0]
+rel = t[:, :, 2] - base
+print("iters", len(t), "blocks", nb)
+print("start skew (max-min) ns: mean %.0f p50 %.0f" % (start.max(1).mean(), np.median(start.max(1))))
+print("work ns per block: mean %.0f, max-over-blocks mean %.0f p50 %.0f p90 %.0f" % (work.mean(), work.max(1).mean(), np.median(work.max(1)), np.percentile(work.max(1), 90)))
+arr = t[:, :, 1] - base
+print("last work end ns (from first start): mean %.0f" % arr.max(1).mean())
+print("release after last work end ns: mean %.0f p50 %.0f" % ((rel.min(1) - arr.max(1)).mean(), np.median(rel.min(1) - arr.max(1))))
+print("release spread ns: mean %.0f" % (rel.max(1) - rel.min(1)).mean())
+nxt = t[1:, :, 0] - t[:-1, :, 2]
+print("release -> next start ns per block: mean %.0f p90 %.0f" % (nxt.mean(), np.percentile(nxt, 90)))
+per = (t[1:, :, 0].min(1) - t[:-1, :, 0].min(1))
+print("iteration period ns: mean %.0f p50 %.0f" % (per.mean(), np.median(per)))
+slow = np.argmax(work, axis=1)
+print("slowest block histogram (top):", np.bincount(slow, minlength=nb).argsort()[::-1][:8], np.sort(np.bincount(slow, minlength=nb))[::-1][:8])

@@ -113,7 +113,28 @@ def test_fps_and_voronoi_exact(name, prec):
     assert np.array_equal(lab, gd[f"voronoi_{p}"])
 
 
+def polar_arrays(spokes, rings, twist=0.37):
+    """Wheel mesh: a centre of valence `spokes` (> 7 exercises the CSR overflow path)."""
+    v = [[0.0, 0.0, 0.0]]
+    for r in range(1, rings + 1):
+        for s in range(spokes):
+            a = 2 * np.pi * s / spokes + twist * r
+            v.append([r * np.cos(a), r * np.sin(a), 0.05 * r * np.sin(3 * a)])
+    f = []
+    ring = lambda r, s: 1 + (r - 1) * spokes + (s % spokes)
+    for s in range(spokes):
+        f.append([0, ring(1, s), ring(1, s + 1)])
+    for r in range(1, rings):
+        for s in range(spokes):
+            a, b, c, d = ring(r, s), ring(r, s + 1), ring(r + 1, s + 1), ring(r + 1, s)
+            f.append([a, d, c])
+            f.append([a, c, b])
+    return np.array(v), np.array(f, np.int32)
+
+
 SYNTH = [
+    ("wheel12", lambda: polar_arrays(12, 9), [[0], [5, 40]]),
+    ("wheel23", lambda: polar_arrays(23, 6), [[0], [3]]),
     ("ico5", lambda: g.icosphere_arrays(5), [[0], [5, 700, 9000]]),
     ("noisy_ico6", lambda: g.noisy_icosphere_arrays(6, 2e-3, 1), [[0], [1, 20000, 33333, 40000]]),
     ("torus64x48", lambda: g.torus_arrays(64, 48), [[0], [17, 1500, 3000]]),
