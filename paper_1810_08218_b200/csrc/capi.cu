@@ -115,12 +115,19 @@ struct Workspace {
     GroupCtl* ctl = nullptr;
     unsigned long long* scratch = nullptr;  // FPS argmax, 2 words per CTA
     int scratch_blocks = 0;
+    int* pring = nullptr;                  // v3 packed records by BFS position
+    void* pL = nullptr;
+    void* pquad = nullptr;
+    unsigned long long* blk_slot = nullptr;  // v3 barrier payload [2][blocks] x 16 B
+    int* blists = nullptr;                 // v3 per-CTA claim lists [2][blocks][claim_cap]
+    int claim_cap = 0;
 
     void release() {
         for (void* p : {dist0, dist1, static_cast<void*>(lab0), static_cast<void*>(lab1),
                         static_cast<void*>(level), static_cast<void*>(queue),
                         static_cast<void*>(limits), static_cast<void*>(ctl),
-                        static_cast<void*>(scratch)})
+                        static_cast<void*>(scratch), static_cast<void*>(pring), pL, pquad,
+                        static_cast<void*>(blk_slot), static_cast<void*>(blists)})
             if (p) cudaFree(p);
         *this = Workspace();
     }
@@ -141,6 +148,32 @@ struct Workspace {
         cuda_ok(cudaMemset(ctl, 0, sizeof(GroupCtl) * g), "memset ctl");
         scratch_blocks = blocks;
         scratch = dalloc<unsigned long long>(2 * static_cast<size_t>(blocks));
+        pring = dalloc<int>(e * kEllW);
+        pL = dalloc<double>(e * kEllW);
+        pquad = dalloc<char>(e * kEllW * 4 * sizeof(double));
+        blk_slot = dalloc<unsigned long long>(4 * static_cast<size_t>(blocks));
+        // a CTA rarely claims more than a few times its share of a level; beyond the
+        // capacity the solve is redone on the general kernel (err 2)
+        claim_cap = static_cast<int>(std::min<long long>(
+            nn + 1, 8 * ((nn + blocks - 1) / std::max(1, blocks / std::max(1, g))) + 4096));
+        blists = dalloc<int>(2 * static_cast<size_t>(blocks) * claim_cap);
+    }
+    void fill(RunArgs& a) const {
+        a.dist0 = dist0;
+        a.dist1 = dist1;
+        a.lab0 = lab0;
+        a.lab1 = lab1;
+        a.level = level;
+        a.queue = queue;
+        a.limits = limits;
+        a.ctl = ctl;
+        a.fps_scratch = scratch;
+        a.pring = pring;
+        a.pL = pL;
+        a.pquad = pquad;
+        a.blk_slot = blk_slot;
+        a.blists = blists;
+        a.claim_cap = claim_cap;
     }
 };
 
@@ -280,6 +313,14 @@ void check_config(const geodist_ptp_config* c) {
         throw std::invalid_argument("precision must be 'single' or 'double'");
 }
 
+// Solver kernel: 2 = queue-based kernel (default), 3 = claimer-first kernel with
+// BFS-ordered packed records (GEODIST_SOLVER=3; falls back to 2 on claim-list
+// overflow).  Tests run both.
+int solver_version() {
+    const char* e = getenv("GEODIST_SOLVER");
+    return (e && e[0] == '3') ? 3 : 2;
+}
+
 // Everything one distance-field solve needs from the caller.
 struct Solve {
     const int32_t* sources = nullptr;
@@ -301,12 +342,16 @@ struct Solve {
     int32_t rho = 0;
 };
 
-void run_solve(geodist_mesh_s* mh, const Solve& q) {
+void run_solve(geodist_mesh_s* mh, const Solve& q, int version);
+
+void run_solve(geodist_mesh_s* mh, const Solve& q) { run_solve(mh, q, solver_version()); }
+
+void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
     const int prec = q.cfg->precision;
     const bool labels = q.m > 1;  // single source: labels are provably inert
     mh->ensure_prec(prec);
     const int n = mh->n;
-    const int maxb = run_max_blocks(prec, labels, mh->device);
+    const int maxb = run_max_blocks(prec, labels, mh->device, version);
     if (maxb <= 0) throw Fail(GEODIST_ECUDA, "run kernel cannot be resident on this device");
     mh->ws.ensure(1, n, maxb);
     Workspace& ws = mh->ws;
@@ -340,15 +385,8 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
     a.mesh.eL = mh->prec[prec].eL;
     a.mesh.equad = mh->prec[prec].equad;
     a.mesh.n = n;
-    a.dist0 = ws.dist0;
-    a.dist1 = ws.dist1;
-    a.lab0 = ws.lab0;
-    a.lab1 = ws.lab1;
-    a.level = ws.level;
-    a.queue = ws.queue;
-    a.limits = ws.limits;
+    ws.fill(a);
     a.stride = n;
-    a.ctl = ws.ctl;
     a.groups = 1;
     a.blocks_per_group = maxb;
     a.src = d_src;
@@ -367,12 +405,11 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
     a.out_labels = d_lab;
     a.qstats = d_qs;
     a.fps_mode = 0;
-    a.fps_scratch = ws.scratch;
     if (const char* e = getenv("GEODIST_DEBUG_TIMING")) {
         a.dbg_iters = atoi(e);
         a.dbg = static_cast<unsigned long long*>(
-            mh->buf(5, sizeof(unsigned long long) * 3 * static_cast<size_t>(a.dbg_iters) * maxb));
-        cuda_ok(cudaMemsetAsync(a.dbg, 0, sizeof(unsigned long long) * 3 * a.dbg_iters * maxb, st),
+            mh->buf(5, sizeof(unsigned long long) * kDbgSlots * static_cast<size_t>(a.dbg_iters) * maxb));
+        cuda_ok(cudaMemsetAsync(a.dbg, 0, sizeof(unsigned long long) * kDbgSlots * a.dbg_iters * maxb, st),
                 "dbg");
     }
 
@@ -384,7 +421,7 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
         a.phase_init = launch == 0 ? 1 : 0;
         a.trace_k0 = hctl.k + 1;
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
-        cuda_ok(launch_run(prec, labels, a, st), "ptp_run_kernel launch");
+        cuda_ok(launch_run(prec, labels, a, st, version), "ptp_run_kernel launch");
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         cuda_ok(cudaMemcpyAsync(&hctl, ws.ctl, sizeof(GroupCtl), cudaMemcpyDeviceToHost, st),
                 "read state");
@@ -415,8 +452,14 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
     }
     QueryStats qs{};
     cuda_ok(cudaMemcpy(&qs, a.qstats, sizeof(QueryStats), cudaMemcpyDeviceToHost), "stats");
+    if (qs.pad == 2 && version == 3) {
+        // a CTA claimed more vertices in one iteration than its shared-memory
+        // list holds: redo the field with the general kernel
+        run_solve(mh, q, 2);
+        return;
+    }
     if (a.dbg) {
-        std::vector<unsigned long long> h(3 * static_cast<size_t>(a.dbg_iters) * maxb);
+        std::vector<unsigned long long> h(kDbgSlots * static_cast<size_t>(a.dbg_iters) * maxb);
         cuda_ok(cudaMemcpy(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost), "dbg");
         if (FILE* f = fopen("gpurun_out/dbg_timing.bin", "wb")) {
             const int hdr[2] = {a.dbg_iters, maxb};
@@ -769,8 +812,10 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
         const int prec = config->precision;
         mh->ensure_prec(prec);
-        const int maxb = std::min(run_max_blocks(prec, true, mh->device),
-                                  run_max_blocks(prec, false, mh->device));
+        int version = solver_version();
+    fps_retry:
+        const int maxb = std::min(run_max_blocks(prec, true, mh->device, version),
+                                  run_max_blocks(prec, false, mh->device, version));
         mh->ws.ensure(1, n, maxb);
         Workspace& ws = mh->ws;
         cudaStream_t st = mh->stream;
@@ -787,15 +832,8 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         a.mesh.eL = mh->prec[prec].eL;
         a.mesh.equad = mh->prec[prec].equad;
         a.mesh.n = n;
-        a.dist0 = ws.dist0;
-        a.dist1 = ws.dist1;
-        a.lab0 = ws.lab0;
-        a.lab1 = ws.lab1;
-        a.level = ws.level;
-        a.queue = ws.queue;
-        a.limits = ws.limits;
+        ws.fill(a);
         a.stride = n;
-        a.ctl = ws.ctl;
         a.groups = 1;
         a.blocks_per_group = maxb;
         a.src = d_samples;
@@ -805,7 +843,6 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         a.phase_init = 1;
         a.max_iters = 0;
         a.fps_mode = 1;
-        a.fps_scratch = ws.scratch;
         a.fps_samples = d_samples;
         a.out_dist = nullptr;
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
@@ -814,7 +851,7 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
             a.fps_final = s == count;
             a.out_labels = s == count ? static_cast<int*>(lab.get()) : nullptr;
             a.qstats = static_cast<QueryStats*>(hist.get()) + (s - 1);
-            cuda_ok(launch_run(prec, s > 1, a, st), "fps round launch");
+            cuda_ok(launch_run(prec, s > 1, a, st, version), "fps round launch");
         }
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         cuda_ok(cudaStreamSynchronize(st), "fps");
@@ -825,6 +862,11 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         cuda_ok(cudaMemcpy(hs.data(), d_samples, sizeof(int) * count, cudaMemcpyDeviceToHost), "d2h");
         cuda_ok(cudaMemcpy(hh.data(), hist.get(), sizeof(QueryStats) * count,
                            cudaMemcpyDeviceToHost), "d2h");
+        if (version == 3 && std::any_of(hh.begin(), hh.end(),
+                                        [](const QueryStats& x) { return x.pad == 2; })) {
+            version = 2;  // claim-list overflow: redo the sampling on the general kernel
+            goto fps_retry;
+        }
         for (int s = 1; s < count; ++s)
             for (int t = 0; t < s; ++t)
                 if (hs[s] == hs[t])
@@ -866,7 +908,9 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         const int prec = config->precision;
         mh->ensure_prec(prec);
         const int n = mh->n;
-        const int maxb = run_max_blocks(prec, multi, mh->device);
+        int version = solver_version();
+    batch_retry:
+        const int maxb = run_max_blocks(prec, multi, mh->device, version);
         int g = groups > 0 ? groups : std::min(nq, 4);
         g = std::max(1, std::min({g, nq, maxb}));
         const int bpg = maxb / g;
@@ -888,15 +932,8 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         a.mesh.eL = mh->prec[prec].eL;
         a.mesh.equad = mh->prec[prec].equad;
         a.mesh.n = n;
-        a.dist0 = ws.dist0;
-        a.dist1 = ws.dist1;
-        a.lab0 = ws.lab0;
-        a.lab1 = ws.lab1;
-        a.level = ws.level;
-        a.queue = ws.queue;
-        a.limits = ws.limits;
+        ws.fill(a);
         a.stride = n;
-        a.ctl = ws.ctl;
         a.groups = g;
         a.blocks_per_group = bpg;
         a.src = static_cast<int*>(srcb.get());
@@ -910,14 +947,18 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         a.out_double = prec == GEODIST_DOUBLE;
         a.out_labels = config->with_labels ? out_labels : nullptr;
         a.qstats = static_cast<QueryStats*>(qs.get());
-        a.fps_scratch = ws.scratch;
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
-        cuda_ok(launch_run(prec, multi, a, st), "batch launch");
+        cuda_ok(launch_run(prec, multi, a, st, version), "batch launch");
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         std::vector<QueryStats> hq(nq);
         cuda_ok(cudaMemcpyAsync(hq.data(), qs.get(), sizeof(QueryStats) * nq,
                                 cudaMemcpyDeviceToHost, st), "d2h");
         cuda_ok(cudaStreamSynchronize(st), "batch");
+        if (version == 3 &&
+            std::any_of(hq.begin(), hq.end(), [](const QueryStats& x) { return x.pad == 2; })) {
+            version = 2;
+            goto batch_retry;
+        }
         float ms = 0.f;
         cudaEventElapsedTime(&ms, mh->ev0, mh->ev1);
         if (out_stats)

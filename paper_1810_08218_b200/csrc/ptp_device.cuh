@@ -31,6 +31,8 @@ constexpr int kMetaShift = 27;     // entry 0 bits 27..30 hold the corner count 
 constexpr int kIdMask = (1 << kMetaShift) - 1;
 constexpr int kEllOverflow = 15;   // d code: more than 7 corners, use the CSR tables
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSlotsPerLane = 8;       // v3: barrier payload slots read per lane of warp 0
+constexpr int kMaxGroupBlocks = 32 * kSlotsPerLane;  // v3: CTAs per query group
 
 // ELL entry e of a vertex lives at slot (e % 4) * 2 + e / 4, so lane l of a
 // 4-lane group reads entries l and l + 4 as one 8-byte (or 16-byte) vector.
@@ -121,6 +123,19 @@ struct RunArgs {
     // (work start, work end after the CTA reduction, barrier release)
     unsigned long long* dbg;
     int dbg_iters;
+    // v3 (claimer-first) solver: BFS-ordered packed records by queue position
+    int* pring;          // 8 ints per position (ELL interleaved)
+    void* pL;            // 8 T per position
+    void* pquad;         // 8 Quad<T> per position
+    unsigned long long* blk_slot;  // [2][gridDim.x][2]: max-rel bits, claim count
+    int* blists;         // [2][gridDim.x][claim_cap] per-CTA claim lists
+    int claim_cap;       // capacity of one claim list
+};
+
+// Per-CTA barrier payload slot (16 B): max relative change bits and claims.
+struct alignas(16) BlkSlot {
+    unsigned long long maxbits;
+    unsigned long long count;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -128,6 +143,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// SM cycle counter read that cannot issue before `dep` is available
+__device__ __forceinline__ unsigned long long gtimer_after(int dep) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "r"(dep));
+    return t;
+}
+__device__ __forceinline__ unsigned long long cyc() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+}
+// [0] start [1] work end [2] release (globaltimer); [3..6] thread-0 task stages,
+// [7] task-loop end, [8..11] barrier3 phases (clock64)
+constexpr int kDbgSlots = 12;
 
 __device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }

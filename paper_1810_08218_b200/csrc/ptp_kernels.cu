@@ -141,6 +141,13 @@ template <> struct Quad<float> {
                                                  float w) {
         static_cast<float4*>(base)[c] = make_float4(x, y, z, w);
     }
+    __device__ __forceinline__ void load_cg(const void* base, size_t c) {
+        const float4 v = __ldcg(static_cast<const float4*>(base) + c);
+        q11 = v.x; q12 = v.y; q22 = v.z; a = v.w;
+    }
+    __device__ __forceinline__ void store_at(void* base, size_t c) const {
+        static_cast<float4*>(base)[c] = make_float4(q11, q12, q22, a);
+    }
 };
 template <> struct Quad<double> {
     double q11, q12, q22, a;
@@ -155,6 +162,16 @@ template <> struct Quad<double> {
         p[0] = make_double2(x, y);
         p[1] = make_double2(z, w);
     }
+    __device__ __forceinline__ void load_cg(const void* base, size_t c) {
+        const double2* p = static_cast<const double2*>(base) + 2 * c;
+        const double2 u = __ldcg(p), w = __ldcg(p + 1);
+        q11 = u.x; q12 = u.y; q22 = w.x; a = w.y;
+    }
+    __device__ __forceinline__ void store_at(void* base, size_t c) const {
+        double2* p = static_cast<double2*>(base) + 2 * c;
+        p[0] = make_double2(q11, q12);
+        p[1] = make_double2(q22, a);
+    }
 };
 
 template <typename T> struct Ell2;
@@ -164,6 +181,15 @@ template <> struct Ell2<float> {
         a = v.x;
         b = v.y;
     }
+    __device__ __forceinline__ static void load_cg(const void* base, size_t at, float& a, float& b) {
+        const float2 v =
+            __ldcg(reinterpret_cast<const float2*>(static_cast<const float*>(base) + at));
+        a = v.x;
+        b = v.y;
+    }
+    __device__ __forceinline__ static void store(void* base, size_t at, float a, float b) {
+        *reinterpret_cast<float2*>(static_cast<float*>(base) + at) = make_float2(a, b);
+    }
 };
 template <> struct Ell2<double> {
     __device__ __forceinline__ static void load(const void* base, size_t at, double& a, double& b) {
@@ -171,6 +197,16 @@ template <> struct Ell2<double> {
             __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(base) + at));
         a = v.x;
         b = v.y;
+    }
+    __device__ __forceinline__ static void load_cg(const void* base, size_t at, double& a,
+                                                   double& b) {
+        const double2 v =
+            __ldcg(reinterpret_cast<const double2*>(static_cast<const double*>(base) + at));
+        a = v.x;
+        b = v.y;
+    }
+    __device__ __forceinline__ static void store(void* base, size_t at, double a, double b) {
+        *reinterpret_cast<double2*>(static_cast<double*>(base) + at) = make_double2(a, b);
     }
 };
 
@@ -249,6 +285,19 @@ __global__ void pack_ell_kernel(int n, const int* __restrict__ cptr,
     }
 }
 
+// Bring a claimed vertex's ELL rows (ring 32 B, |x| 32/64 B, quads 128/256 B)
+// into L2 one iteration before its first relaxation reads them.
+template <typename T>
+__device__ __forceinline__ void prefetch_ell(const MeshDev& M, int v) {
+    const size_t eb = static_cast<size_t>(v) * kEllW;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(M.ering + eb));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const T*>(M.eL) + eb));
+    const char* q = static_cast<const char*>(M.equad) + eb * 4 * sizeof(T);
+#pragma unroll
+    for (int o = 0; o < static_cast<int>(kEllW * 4 * sizeof(T)); o += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(q + o));
+}
+
 // ---------------------------------------------------------------------------
 // group barrier (all CTAs of one query): release-add arrival, acquire polling.
 // Thread 0 runs `post` after the release, before the closing __syncthreads.
@@ -260,8 +309,8 @@ template <typename Post>
 __device__ __forceinline__ void group_barrier(unsigned* bar, unsigned& epoch, unsigned nblk,
                                               Post&& post) {
     __syncthreads();
+    ++epoch;  // every thread tracks the epoch (barrier3 polls from all of warp 0)
     if (threadIdx.x == 0) {
-        ++epoch;
         red_release(bar, 1u);
         const unsigned target = epoch * nblk;
         while (static_cast<int>(ld_acquire(bar) - target) < 0) {
@@ -430,6 +479,8 @@ __device__ __forceinline__ void relax_group(const MeshDev& M, bool act, int p, i
     int blab = gl == 0 ? lv : -1;
     chunk_candidates<T, LABELS>(gl, 0, ovf ? 0 : d, rr.x, rr.y, La, Lb, ta, tb, la, lb_, qa, qb,
                                 best, bidx, blab, degs);
+    if (ca_claim) prefetch_ell<T>(M, ida);
+    if (cb_claim) prefetch_ell<T>(M, idb);
     append_claims(ca_claim, ida, tail_ptr, queue_w);
     append_claims(cb_claim, idb, tail_ptr, queue_w);
 
@@ -685,7 +736,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
             const int kk = S.k;
             const bool dbg = A.dbg != nullptr && tid == 0 && iters < A.dbg_iters;
             unsigned long long* dslot =
-                dbg ? A.dbg + 3 * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
+                dbg ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
             if (dbg) dslot[0] = gtimer();
             const int prv = S.parity, cur = prv ^ 1;
             const T* dp = dist[prv];
@@ -857,6 +908,679 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
     }
 }
 
+// ===========================================================================
+// v3 solver: claimer-first relaxation over BFS-ordered packed records.
+//
+// A CTA that claims vertices for level k+1 (during iteration k) appends their
+// ids to its own global claim list (index from a shared-memory counter, no
+// global atomic).  The per-CTA claim counts ride on the grid barrier together
+// with the per-CTA max relative change; every CTA turns them into a prefix
+// table, which maps the new level's BFS positions to (claimer, index).  At
+// iteration k+1 the new level is relaxed round-robin like the rest of the band:
+// a task of the new level looks its id up in the claimer's list, relaxes it from
+// the id-indexed ELL tables and writes the vertex's packed record (id, ring,
+// |x|, Gram quads) at its BFS position; older band levels are relaxed straight
+// from those packed records -- the reference's reorder_for_bands layout
+// (toplesets.cpp:60-89), built incrementally while the band advances.  A task
+// costs two dependent L2 round trips (record, then neighbour distances), three
+// for the newest level (claim-list lookup first).
+// ===========================================================================
+
+struct Bcast3 {
+    int k, i, j, bb, oe, be, fe, frzb, frze, parity, done, cur, expand;
+};
+
+__device__ __forceinline__ void ld_acquire_v2(const unsigned long long* p, unsigned long long& a,
+                                              unsigned long long& b) {
+    asm volatile("ld.acquire.gpu.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(a), "=l"(b)
+                 : "l"(p)
+                 : "memory");
+}
+
+// Warp-aggregated append of claims (entries a and b of every lane) to the
+// CTA's own global claim list for the next level (index from a shared-memory
+// counter: no global atomic).
+__device__ __forceinline__ void list_claims(bool ca, int ia, bool cb, int ib, int* list,
+                                            int* cnt, int cap, int* err) {
+    const unsigned ba = __ballot_sync(kFull, ca), bbal = __ballot_sync(kFull, cb);
+    if ((ba | bbal) == 0u) return;
+    const int l32 = threadIdx.x & 31;
+    const int leader = __ffs(ba | bbal) - 1;
+    int base = 0;
+    if (l32 == leader) base = atomicAdd(cnt, __popc(ba) + __popc(bbal));
+    base = __shfl_sync(kFull, base, leader);
+    const unsigned lt = (1u << l32) - 1u;
+    if (ca) {
+        const int at = base + __popc(ba & lt);
+        if (at < cap) list[at] = ia; else *err = 2;
+    }
+    if (cb) {
+        const int at = base + __popc(ba) + __popc(bbal & lt);
+        if (at < cap) list[at] = ib; else *err = 2;
+    }
+}
+
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax3(const MeshDev& M, const RunArgs& A, long long off8,
+                                       bool act, bool is_new, int v_new, int p, int kk,
+                                       int* pv, const T* dp, T* dc, const int* lp, int* lc,
+                                       int fe, bool expand, int* level, int* nlist, int* ncnt,
+                                       int* err, T eps, T& my_max, long long& calls,
+                                       long long& degs, unsigned long long* tdbg) {
+    const T inf = Lim<T>::inf();
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int g0 = (threadIdx.x & 31) & ~(kGroup - 1);
+    if (tdbg) tdbg[3] = cyc();
+    int* pring = A.pring + off8;
+    T* pL = static_cast<T*>(A.pL) + off8;
+    char* pquad = static_cast<char*>(A.pquad) + off8 * sizeof(Quad<T>);
+    const size_t pb = static_cast<size_t>(p) * kEllW;
+    int v = 0;
+    int2 rr = make_int2(0, 0);
+    T La = T(0), Lb = T(0);
+    Quad<T> qa, qb;
+    qa.q11 = qa.q12 = qa.q22 = qa.a = T(0);
+    qb = qa;
+    if (act) {
+        if (is_new) {
+            v = v_new;
+            const size_t eb = static_cast<size_t>(v) * kEllW;
+            rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
+            Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
+            qa.load(M.equad, static_cast<int>(eb + 2 * gl));
+            qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
+            // commit the packed record at the vertex's BFS position
+            if (gl == 0) pv[p] = v;
+            reinterpret_cast<int2*>(pring)[(pb >> 1) + gl] = rr;
+            Ell2<T>::store(pL, pb + 2 * gl, La, Lb);
+            qa.store_at(pquad, pb + 2 * gl);
+            qb.store_at(pquad, pb + 2 * gl + 1);
+        } else {
+            v = ldcg(pv + p);
+            rr = __ldcg(reinterpret_cast<const int2*>(pring) + (pb >> 1) + gl);
+            Ell2<T>::load_cg(pL, pb + 2 * gl, La, Lb);
+            qa.load_cg(pquad, pb + 2 * gl);
+            qb.load_cg(pquad, pb + 2 * gl + 1);
+        }
+    }
+    if (tdbg) tdbg[4] = gtimer_after(rr.x + v);
+    const int meta = __shfl_sync(kFull, rr.x, g0);
+    int d = act ? (meta >> kMetaShift) & 15 : 0;
+    const bool ovf = d == kEllOverflow;
+    const int ida = rr.x & kIdMask, idb = rr.y & kIdMask;
+    const bool hasa = act && !ovf && d > 0 && gl <= d;
+    const bool hasb = act && !ovf && d > 0 && gl + kGroup <= d;
+    const bool exp = expand && is_new;
+    bool ca_claim = false, cb_claim = false;
+    if (exp) {
+        if (hasa) ca_claim = atomicCAS(level + ida, -1, kk + 1) == -1;
+        if (hasb) cb_claim = atomicCAS(level + idb, -1, kk + 1) == -1;
+    }
+    T tv = inf;
+    int lv = -1;
+    if (act) {
+        tv = ldcg(dp + v);
+        if (LABELS) lv = ldcg(lp + v);
+    }
+    T ta = inf, tb = inf;
+    int la = -1, lb_ = -1;
+    if (hasa) {
+        ta = ldcg(dp + ida);
+        if (LABELS) la = ldcg(lp + ida);
+    }
+    if (hasb) {
+        tb = ldcg(dp + idb);
+        if (LABELS) lb_ = ldcg(lp + idb);
+    }
+    if (tdbg) tdbg[5] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv)));
+    T best = gl == 0 ? tv : inf;
+    int bidx = gl == 0 ? -1 : INT_MAX;
+    int blab = gl == 0 ? lv : -1;
+    chunk_candidates<T, LABELS>(gl, 0, ovf ? 0 : d, rr.x, rr.y, La, Lb, ta, tb, la, lb_, qa, qb,
+                                best, bidx, blab, degs);
+    if (tdbg) tdbg[6] = gtimer_after(__float_as_int(static_cast<float>(best)) + ca_claim + cb_claim);
+    if (ca_claim) prefetch_ell<T>(M, ida);
+    if (cb_claim) prefetch_ell<T>(M, idb);
+    list_claims(ca_claim, ida, cb_claim, idb, nlist, ncnt, A.claim_cap, err);
+
+    // overflow vertices (> 7 corners): CSR tables, 7 corners per chunk
+    if (__any_sync(kFull, act && ovf)) {
+        int c0 = 0;
+        if (act && ovf) {
+            c0 = __ldg(M.cptr + v);
+            d = __ldg(M.cptr + v + 1) - c0;
+        }
+        const int r0 = c0 + v;
+        int nch = act && ovf ? (d + kEllW - 2) / (kEllW - 1) : 0;
+        nch = __reduce_max_sync(kFull, nch);
+        const int* ring = M.ring;
+        const T* ringL = static_cast<const T*>(M.ringL);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int base = ch * (kEllW - 1);
+            const int ea = base + gl, ebb = base + gl + kGroup;
+            const bool ha = act && ovf && ea <= d, hb = act && ovf && ebb <= d;
+            int xa = 0, xb = 0;
+            T LA = T(0), LB = T(0), TA = inf, TB = inf;
+            int lA = -1, lB = -1;
+            Quad<T> QA, QB;
+            QA.q11 = QA.q12 = QA.q22 = QA.a = T(0);
+            QB = QA;
+            if (ha) {
+                xa = __ldg(ring + r0 + ea);
+                LA = __ldg(ringL + r0 + ea);
+                if (ea < d) QA.load(M.quad, c0 + ea);
+            }
+            if (hb) {
+                xb = __ldg(ring + r0 + ebb);
+                LB = __ldg(ringL + r0 + ebb);
+                if (ebb < d) QB.load(M.quad, c0 + ebb);
+            }
+            const int ia = xa & INT_MAX, ib = xb & INT_MAX;
+            bool cA = false, cB = false;
+            if (exp) {
+                if (ha) cA = atomicCAS(level + ia, -1, kk + 1) == -1;
+                if (hb) cB = atomicCAS(level + ib, -1, kk + 1) == -1;
+            }
+            if (ha) {
+                TA = ldcg(dp + ia);
+                if (LABELS) lA = ldcg(lp + ia);
+            }
+            if (hb) {
+                TB = ldcg(dp + ib);
+                if (LABELS) lB = ldcg(lp + ib);
+            }
+            const int dlim = act && ovf ? min(d, base + kEllW - 1) : 0;
+            chunk_candidates<T, LABELS>(gl, base, dlim, xa, xb, LA, LB, TA, TB, lA, lB, QA, QB,
+                                        best, bidx, blab, degs);
+            list_claims(cA, ia, cB, ib, nlist, ncnt, A.claim_cap, err);
+        }
+    }
+
+    for (int o = kGroup / 2; o > 0; o >>= 1) {
+        const T ob = __shfl_xor_sync(kFull, best, o, kGroup);
+        const int oi = __shfl_xor_sync(kFull, bidx, o, kGroup);
+        int ol = -1;
+        if (LABELS) ol = __shfl_xor_sync(kFull, blab, o, kGroup);
+        if (ob < best || (ob == best && oi < bidx)) {
+            best = ob;
+            bidx = oi;
+            if (LABELS) blab = ol;
+        }
+    }
+    if (act && gl == 0) {
+        dc[v] = best;
+        if (LABELS) lc[v] = blab;
+        calls += d;
+        const T rc = rel_change(tv, best);
+        if (p < fe && rc > my_max) my_max = rc;
+        if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
+    }
+}
+
+template <typename T, bool LABELS>
+__global__ void __launch_bounds__(kBlock, 1) ptp_run3_kernel(RunArgs A) {
+    __shared__ Bcast3 S;
+    __shared__ int s_pref[kMaxGroupBlocks + 1];  // prefix of last iteration's claim counts
+    __shared__ T red_t[kBlock / 32];
+    __shared__ long long red_l[kBlock / 32];
+    __shared__ double red_v[kBlock / 32];
+    __shared__ int red_i[kBlock / 32];
+    __shared__ int s_ncnt, s_err;
+
+    const int tid = threadIdx.x;
+    const int nb = A.blocks_per_group;
+    const int g = blockIdx.x / nb;
+    const int lb = blockIdx.x - g * nb;
+    GroupCtl* ctl = A.ctl + g;
+    const long long off = static_cast<long long>(g) * A.stride;
+    const long long off8 = off * kEllW;
+    T* dist[2] = {static_cast<T*>(A.dist0) + off, static_cast<T*>(A.dist1) + off};
+    int* lab[2] = {nullptr, nullptr};
+    if (LABELS) {
+        lab[0] = A.lab0 + off;
+        lab[1] = A.lab1 + off;
+    }
+    int* level = A.level + off;
+    int* pv = A.queue + off;
+    int* limits = A.limits + off;
+    // this CTA's claim lists (parity 0/1) and the base of all lists of the group
+    int* lists[2] = {A.blists + (static_cast<size_t>(0) * gridDim.x + blockIdx.x) * A.claim_cap,
+                     A.blists + (static_cast<size_t>(1) * gridDim.x + blockIdx.x) * A.claim_cap};
+    auto claim_list = [&](int par, int b) {
+        return A.blists + (static_cast<size_t>(par) * gridDim.x + g * nb + b) * A.claim_cap;
+    };
+    const MeshDev M = A.mesh;
+    const int n = M.n;
+    const T inf = Lim<T>::inf();
+    const T eps = static_cast<T>(A.eps);
+    unsigned epoch = 0;
+    const int gthreads = nb * kBlock;
+    const int gtid = lb * kBlock + tid;
+    constexpr int kGroupsPerBlock = kBlock / kGroup;
+    BlkSlot* slots = reinterpret_cast<BlkSlot*>(A.blk_slot);  // [2][gridDim.x]
+
+    // grid barrier whose payload (per-CTA max and claim count) is reduced by warp 0
+    unsigned long long* bdbg = nullptr;  // barrier3 phase timers (debug)
+    auto barrier3 = [&](int par, unsigned long long mybits, int mycnt, auto&& post) {
+        if (tid == 0) {
+            BlkSlot sl;
+            sl.maxbits = mybits;
+            sl.count = static_cast<unsigned long long>(mycnt);
+            __stcg(reinterpret_cast<ulonglong2*>(&slots[par * gridDim.x + blockIdx.x]),
+                   make_ulonglong2(sl.maxbits, sl.count));
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // every lane of warp 0 polls with acquire semantics (one coalesced
+            // request per poll), so its relaxed slot reads below are ordered
+            ++epoch;
+            if (tid == 0 && bdbg) bdbg[8] = cyc();
+            if (tid == 0) red_release(&ctl->bar, 1u);
+            if (tid == 0 && bdbg) bdbg[9] = cyc();
+            const unsigned target = epoch * nb;
+            while (static_cast<int>(ld_acquire(&ctl->bar) - target) < 0) {
+            }
+            if (tid == 0 && bdbg) bdbg[10] = cyc();
+            // lane l reads CTAs [l*per, (l+1)*per): max, and an exclusive scan of
+            // the claim counts into s_pref (block order)
+            const int per = (nb + 31) / 32;
+            const int b0 = tid * per, b1 = min(nb, b0 + per);
+            unsigned long long mx = 0, mine = 0;
+            ulonglong2 sv[kSlotsPerLane];
+#pragma unroll
+            for (int x = 0; x < kSlotsPerLane; ++x)  // all loads in flight at once
+                if (b0 + x < b1)
+                    sv[x] = __ldcg(reinterpret_cast<const ulonglong2*>(
+                        &slots[par * gridDim.x + g * nb + b0 + x]));
+#pragma unroll
+            for (int x = 0; x < kSlotsPerLane; ++x)
+                if (b0 + x < b1) {
+                    mx = sv[x].x > mx ? sv[x].x : mx;
+                    s_pref[b0 + x] = static_cast<int>(sv[x].y);
+                    mine += sv[x].y;
+                }
+            unsigned long long incl = mine;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+                if (tid >= o) incl += y;
+            }
+            unsigned long long run = incl - mine;
+            for (int b = b0; b < b1; ++b) {
+                const int c = s_pref[b];
+                s_pref[b] = static_cast<int>(run);
+                run += c;
+            }
+            const unsigned long long tot = __shfl_sync(kFull, incl, 31);
+            if (tid == 0) s_pref[nb] = static_cast<int>(tot);
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(kFull, mx, o);
+                mx = y > mx ? y : mx;
+            }
+            __syncwarp();
+            const unsigned long long before = static_cast<unsigned long long>(s_pref[lb]);
+            if (tid == 0 && bdbg) bdbg[11] = cyc();
+            if (tid == 0) post(mx, static_cast<int>(tot), static_cast<int>(before));
+        }
+        __syncthreads();
+    };
+
+    for (int q = g; q < A.nq; q += A.groups) {
+        const int s0 = A.src_off ? A.src_off[q] : 0;
+        const int m = A.src_off ? A.src_off[q + 1] - s0 : A.src_count;
+        const int* src = A.src + s0;
+        int k = 0, i = 1, rho = INT_MAX, parity = 0, bfs_open = 0, done = 0;
+        int tail = 0, limk = 0, bb = 0, fe = 0, frzb = 0, frze = 0;
+        unsigned long long upd = 0;
+        int pf = -1;
+        auto publish = [&] {
+            S.done = done;
+            s_ncnt = 0;
+            if (done) return;
+            const int kk = k + 1;
+            const int j = bfs_open ? kk : min(kk, rho - 1);
+            S.k = kk;
+            S.i = i;
+            S.j = j;
+            S.bb = bb;
+            S.fe = fe;
+            const int be = (bfs_open || j + 1 == rho) ? tail : ldcg(limits + j + 1);
+            S.be = be;
+            S.oe = bfs_open ? limk : be;  // newest level: ids from the claim lists
+            S.expand = bfs_open;
+            S.cur = k & 1;                // claim-list parity holding the newest level
+            S.frzb = frzb;
+            S.frze = frze;
+            S.parity = parity;
+            pf = -1;
+            if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
+                pf = (bfs_open && i + 2 == kk + 1) ? tail : ldcg(limits + i + 2);
+        };
+
+        if (tid == 0) s_err = 0;
+        if (A.phase_init) {
+            for (int v = gtid; v < n; v += gthreads) {
+                dist[0][v] = inf;
+                dist[1][v] = inf;
+                if (LABELS) {
+                    lab[0][v] = -1;
+                    lab[1][v] = -1;
+                }
+                if (A.fused_bfs) level[v] = -1;
+                if (A.last_change) A.last_change[v] = 0;
+            }
+            if (gtid == 0) {
+                ctl->relax = ctl->degen = ctl->updates = 0;
+                ctl->err = 0;
+            }
+            group_barrier(&ctl->bar, epoch, nb, [] {});
+            for (int s = gtid; s < m; s += gthreads) {
+                const int v = src[s];
+                dist[0][v] = T(0);
+                dist[1][v] = T(0);
+                if (LABELS) {
+                    lab[0][v] = s;
+                    lab[1][v] = s;
+                }
+                if (A.fused_bfs) {
+                    level[v] = 0;
+                    pv[s] = v;
+                }
+            }
+            if (A.fused_bfs && gtid == 0) {
+                limits[0] = 0;
+                limits[1] = m;
+            }
+            if (!A.fused_bfs) {
+                // caller ordering: pack every reachable position's record up front
+                const int reach = ldcg(limits + A.given_rho);
+                int* pring = A.pring + off8;
+                T* pL = static_cast<T*>(A.pL) + off8;
+                char* pquad = static_cast<char*>(A.pquad) + off8 * sizeof(Quad<T>);
+                for (long long x = gtid; x < static_cast<long long>(reach) * kEllW;
+                     x += gthreads) {
+                    const int p = static_cast<int>(x / kEllW), slot = static_cast<int>(x % kEllW);
+                    const int v = ldcg(pv + p);
+                    const size_t eb = static_cast<size_t>(v) * kEllW + slot;
+                    pring[x] = __ldg(M.ering + eb);
+                    pL[x] = __ldg(static_cast<const T*>(M.eL) + eb);
+                    Quad<T> qq;
+                    qq.load(M.equad, static_cast<int>(eb));
+                    qq.store_at(pquad, x);
+                }
+            }
+            if (tid == 0) s_ncnt = 0;
+            group_barrier(&ctl->bar, epoch, nb, [] {});
+            if (A.fused_bfs) {
+                // iteration 0: claim level 1 from the sources into list 0
+                const int gl = tid & (kGroup - 1);
+                for (int t = lb + nb * (tid / kGroup);; t += nb * kGroupsPerBlock) {
+                    const bool act = t < m;
+                    if (!__any_sync(kFull, act)) break;
+                    int v = 0, c0 = 0, d = 0;
+                    if (act) {
+                        v = ldcg(pv + t);
+                        c0 = __ldg(M.cptr + v);
+                        d = __ldg(M.cptr + v + 1) - c0;
+                    }
+                    int nch = d > 0 ? (d + 2 * kGroup) / (2 * kGroup) : 0;  // entries 0..d
+                    nch = __reduce_max_sync(kFull, nch);
+                    for (int ch = 0; ch < nch; ++ch) {
+                        const int ea = ch * 2 * kGroup + gl, eb2 = ea + kGroup;
+                        bool cA = false, cB = false;
+                        int ia = 0, ib = 0;
+                        if (act && d > 0 && ea <= d) {
+                            ia = __ldg(M.ring + c0 + v + ea) & INT_MAX;
+                            cA = atomicCAS(level + ia, -1, 1) == -1;
+                        }
+                        if (act && d > 0 && eb2 <= d) {
+                            ib = __ldg(M.ring + c0 + v + eb2) & INT_MAX;
+                            cB = atomicCAS(level + ib, -1, 1) == -1;
+                        }
+                        list_claims(cA, ia, cB, ib, lists[0], &s_ncnt, A.claim_cap, &s_err);
+                    }
+                }
+                __syncthreads();
+                const int mycnt = s_ncnt;
+                barrier3(0, 0ull, mycnt, [&](unsigned long long, int tot, int) {
+                    bb = m;
+                    if (tot == 0) {
+                        bfs_open = 0;
+                        rho = 1;
+                        tail = m;
+                        fe = m;
+                    } else {
+                        bfs_open = 1;
+                        limk = m;
+                        tail = m + tot;
+                        fe = tail;
+                        if (lb == 0) limits[2] = tail;
+                    }
+                    done = !bfs_open && i > rho - 1;
+                    publish();
+                });
+            } else {
+                if (tid == 0) {
+                    rho = A.given_rho;
+                    bfs_open = 0;
+                    tail = ldcg(limits + rho);
+                    bb = ldcg(limits + 1);
+                    fe = rho >= 2 ? ldcg(limits + 2) : tail;
+                    done = i > rho - 1;
+                    publish();
+                }
+                __syncthreads();
+            }
+        } else {
+            if (tid == 0) {
+                k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
+                bfs_open = ctl->bfs_open; done = ctl->done;
+                tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
+                frzb = ctl->s_frzb; frze = ctl->s_frze;
+                publish();
+            }
+            __syncthreads();
+        }
+
+        T my_max = T(0);
+        long long calls = 0, degs = 0;
+        int iters = 0;
+        for (;;) {
+            if (S.done || (A.max_iters > 0 && iters >= A.max_iters)) break;
+            const int kk = S.k;
+            const bool dbg = A.dbg != nullptr && tid == 0 && iters < A.dbg_iters;
+            unsigned long long* dslot =
+                dbg ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
+            if (dbg) dslot[0] = gtimer();
+            const int prv = S.parity, cur_b = prv ^ 1;
+            const T* dp = dist[prv];
+            T* dcur = dist[cur_b];
+            const int* lp = LABELS ? lab[prv] : nullptr;
+            int* lc = LABELS ? lab[cur_b] : nullptr;
+            const int bb_ = S.bb, fe_ = S.fe, oe_ = S.oe;
+            const bool expand = S.expand != 0;
+            const int* clist_base = claim_list(S.cur, 0);
+            int* nlist = lists[kk & 1];
+            const int ntask = S.be - bb_;
+            my_max = T(0);
+            for (int t = lb + nb * (tid / kGroup);; t += nb * kGroupsPerBlock) {
+                const bool act = t < ntask;
+                if (!__any_sync(kFull, act)) break;
+                const int p = bb_ + t;
+                const bool is_new = p >= oe_;
+                int vn = 0;
+                if (act && is_new) {
+                    // position -> (claimer CTA, index) through the prefix table
+                    const int r = p - oe_;
+                    int lo = 0, hi = nb;  // s_pref[lo] <= r < s_pref[hi]
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s_pref[mid] <= r) lo = mid; else hi = mid;
+                    }
+                    vn = ldcg(clist_base + static_cast<size_t>(lo) * A.claim_cap + (r - s_pref[lo]));
+                }
+                relax3<T, LABELS>(M, A, off8, act, is_new, vn, p, kk, pv, dp, dcur, lp, lc, fe_,
+                                  expand, level, nlist, &s_ncnt, &s_err, eps, my_max, calls, degs,
+                                  (dbg && t == lb && act) ? dslot : nullptr);
+            }
+            if (dbg) dslot[7] = cyc();
+            // deferred freeze of the level retired last iteration, on the highest
+            // (usually idle) threads (ptp.cpp:121-130)
+            {
+                const int nf = S.frze - S.frzb;
+                for (int f = gthreads - 1 - gtid; f < nf; f += gthreads) {
+                    const int v = ldcg(pv + S.frzb + f);
+                    dcur[v] = ldcg(dp + v);
+                    if (LABELS) lc[v] = ldcg(lp + v);
+                }
+            }
+            const T bmax = block_max(my_max, red_t);
+            if (dbg) dslot[1] = gtimer();
+            bdbg = dslot;
+            const int mycnt = s_ncnt;  // after block_max's __syncthreads
+            barrier3(kk & 1, Lim<T>::bits(bmax), mycnt,
+                     [&](unsigned long long mxb, int tot, int) {
+                if (dbg) dslot[2] = gtimer();
+                const T mr = Lim<T>::from_bits(mxb);
+                const bool conv = mr < eps;  // ptp.cpp:114
+                const int ub = bb, ue = S.be;
+                upd += static_cast<unsigned long long>(ue - ub);
+                if (lb == 0 && A.trace != nullptr) {
+                    const int row = kk - A.trace_k0;
+                    if (row >= 0 && row < A.trace_cap) {
+                        TraceRow r;
+                        r.k = kk; r.i = i; r.j = S.j; r.conv = conv ? 1 : 0;
+                        r.updated = ue - ub;
+                        r.max_rel = static_cast<double>(mr);
+                        A.trace[row] = r;
+                    }
+                }
+                int nt = tail;
+                if (bfs_open) {
+                    if (tot == 0) {
+                        bfs_open = 0;
+                        rho = kk + 1;
+                    } else {
+                        nt = tail + tot;
+                        if (lb == 0) limits[kk + 2] = nt;
+                        limk = tail;
+                    }
+                }
+                if (conv) {
+                    frzb = bb;
+                    frze = fe;
+                    bb = fe;
+                    fe = (i + 2 <= kk + 1) ? pf : nt;
+                    ++i;
+                } else {
+                    frzb = frze = 0;
+                }
+                tail = nt;
+                parity ^= 1;
+                k = kk;
+                done = !bfs_open && i > rho - 1;
+                publish();
+            });
+            ++iters;
+        }
+
+        const long long bc = block_sum(calls, red_l);
+        const long long bd = block_sum(degs, red_l);
+        if (tid == 0) {
+            if (bc) atomicAdd(&ctl->relax, static_cast<unsigned long long>(bc));
+            if (bd) atomicAdd(&ctl->degen, static_cast<unsigned long long>(bd));
+            if (s_err) atomicMax(&ctl->err, s_err);
+            if (lb == 0) {
+                ctl->k = k; ctl->i = i; ctl->rho = rho; ctl->parity = parity;
+                ctl->bfs_open = bfs_open; ctl->done = done;
+                ctl->s_tail = tail; ctl->s_limk = limk; ctl->s_bb = bb; ctl->s_fe = fe;
+                ctl->s_frzb = frzb; ctl->s_frze = frze;
+                ctl->updates += upd;
+            }
+            S.done = done;
+            S.parity = parity;
+        }
+        __syncthreads();
+        const int fin_done = S.done;
+        const int fin = S.parity;
+        if (!fin_done) continue;
+
+        double vmax = -1.0;
+        int vidx = INT_MAX;
+        if (A.out_dist != nullptr || A.fps_mode || A.out_labels != nullptr) {
+            const T* df = dist[fin];
+            const int* lf = LABELS ? lab[fin] : nullptr;
+            const long long qo = static_cast<long long>(q) * n;
+            for (int v = gtid; v < n; v += gthreads) {
+                const T x = ldcg(df + v);
+                if (A.out_dist != nullptr) {
+                    if (A.out_double)
+                        static_cast<double*>(A.out_dist)[qo + v] = static_cast<double>(x);
+                    else
+                        static_cast<float*>(A.out_dist)[qo + v] = static_cast<float>(x);
+                }
+                if (A.out_labels != nullptr)
+                    A.out_labels[qo + v] = LABELS ? ldcg(lf + v) : (x != inf ? 0 : -1);
+                const double xd = static_cast<double>(x);
+                if (xd > vmax || (xd == vmax && v < vidx)) {
+                    vmax = xd;
+                    vidx = v;
+                }
+            }
+        }
+        if (A.fps_mode) {
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(kFull, vmax, o);
+                const int oi = __shfl_xor_sync(kFull, vidx, o);
+                if (ov > vmax || (ov == vmax && oi < vidx)) { vmax = ov; vidx = oi; }
+            }
+            if ((tid & 31) == 0) { red_v[tid >> 5] = vmax; red_i[tid >> 5] = vidx; }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < kBlock / 32; ++w)
+                    if (red_v[w] > vmax || (red_v[w] == vmax && red_i[w] < vidx)) {
+                        vmax = red_v[w];
+                        vidx = red_i[w];
+                    }
+                A.fps_scratch[2 * blockIdx.x] =
+                    static_cast<unsigned long long>(__double_as_longlong(vmax));
+                A.fps_scratch[2 * blockIdx.x + 1] = static_cast<unsigned long long>(vidx);
+            }
+        }
+        group_barrier(&ctl->bar, epoch, nb, [&] {
+            if (lb != 0) return;
+            QueryStats st;
+            st.relax = static_cast<long long>(__ldcg(&ctl->relax));
+            st.degen = static_cast<long long>(__ldcg(&ctl->degen));
+            st.updates = static_cast<long long>(ctl->updates);
+            st.iterations = k;
+            st.rho = rho;
+            st.unreached = n - tail;
+            st.done = 1;
+            st.radius = 0.0;
+            st.argmax = -1;
+            st.pad = 0;
+            if (A.fps_mode) {
+                double bv = -1.0;
+                int bi = INT_MAX;
+                for (int b = g * nb; b < g * nb + nb; ++b) {
+                    const double ov = __longlong_as_double(
+                        static_cast<long long>(__ldcg(&A.fps_scratch[2 * b])));
+                    const int oi = static_cast<int>(__ldcg(&A.fps_scratch[2 * b + 1]));
+                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                st.radius = bv;
+                st.argmax = bi;
+                if (!A.fps_final) {
+                    if (ldcg(level + bi) == 0) ctl->err = 1;
+                    A.fps_samples[A.src_count] = bi;
+                }
+            }
+            A.qstats[q] = st;
+        });
+    }
+}
+
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void planar_test_kernel(const double* x1, const double* x2, const double* t1,
@@ -915,31 +1639,47 @@ __global__ void reset_bars_kernel(GroupCtl* ctl, int groups) {
     for (int g = threadIdx.x; g < groups; g += blockDim.x) ctl[g].bar = 0u;
 }
 
-static const void* run_kernel_ptr(int precision, bool labels) {
+static const void* run_kernel_ptr(int version, int precision, bool labels) {
+    if (version == 2) {
+        if (precision == 0)
+            return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<float, true>)
+                          : reinterpret_cast<const void*>(&ptp_run_kernel<float, false>);
+        return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<double, true>)
+                      : reinterpret_cast<const void*>(&ptp_run_kernel<double, false>);
+    }
     if (precision == 0)
-        return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<float, true>)
-                      : reinterpret_cast<const void*>(&ptp_run_kernel<float, false>);
-    return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<double, true>)
-                  : reinterpret_cast<const void*>(&ptp_run_kernel<double, false>);
+        return labels ? reinterpret_cast<const void*>(&ptp_run3_kernel<float, true>)
+                      : reinterpret_cast<const void*>(&ptp_run3_kernel<float, false>);
+    return labels ? reinterpret_cast<const void*>(&ptp_run3_kernel<double, true>)
+                  : reinterpret_cast<const void*>(&ptp_run3_kernel<double, false>);
 }
 
-int run_max_blocks(int precision, bool labels, int device) {
+static size_t run_dyn_smem(int) { return 0; }
+
+int run_max_blocks(int precision, bool labels, int device, int version) {
     int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run_kernel_ptr(precision, labels),
-                                                  kBlock, 0);
+    const void* f = run_kernel_ptr(version, precision, labels);
+    const size_t dyn = run_dyn_smem(version);
+    if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kBlock, dyn);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return per_sm * sms;
+    const int total = per_sm * sms;
+    return version == 3 ? (total < kMaxGroupBlocks ? total : kMaxGroupBlocks) : total;
 }
 
-cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st) {
+cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st,
+                       int version) {
     const int grid = args.groups * args.blocks_per_group;
-    void* params[] = {const_cast<RunArgs*>(&args)};
-    reset_bars_kernel<<<1, 32, 0, st>>>(args.ctl, args.groups);
+    RunArgs a = args;
+    void* params[] = {&a};
+    reset_bars_kernel<<<1, 32, 0, st>>>(a.ctl, a.groups);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    e = cudaLaunchCooperativeKernel(run_kernel_ptr(precision, labels), dim3(grid), dim3(kBlock),
-                                    params, 0, st);
+    const void* f = run_kernel_ptr(version, precision, labels);
+    const size_t dyn = run_dyn_smem(version);
+    if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    e = cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kBlock), params, dyn, st);
     note_launch();
     return e;
 }

@@ -19,8 +19,11 @@ void launch_planar_test(int precision, const double* x1, const double* x2, const
                         cudaStream_t st);
 
 // Max co-resident CTAs of the run kernel on `device` (cooperative launch bound).
-int run_max_blocks(int precision, bool labels, int device);
-cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st);
+// version 3: claimer-first solver (default); version 2: general queue-based solver
+// (used when a CTA's claims overflow its shared-memory list).
+int run_max_blocks(int precision, bool labels, int device, int version = 3);
+cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st,
+                       int version = 3);
 
 // Toplesets with the reference's exact ordering (toplesets.cu).
 struct TopoArgs {

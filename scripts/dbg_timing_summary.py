@@ -1,7 +1,7 @@
 import numpy as np, sys
 raw = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/dbg_timing.bin", "rb").read()
 it, nb = np.frombuffer(raw[:8], np.int32)
-t = np.frombuffer(raw[8:], np.uint64).reshape(it, nb, 3).astype(np.int64)
+t = np.frombuffer(raw[8:], np.uint64).reshape(it, nb, 12).astype(np.int64)
 valid = (t[:, :, 0] > 0).all(axis=1)
 t = t[valid]
 base = t[:, :, 0].min(axis=1, keepdims=True)
@@ -21,3 +21,19 @@ per = (t[1:, :, 0].min(1) - t[:-1, :, 0].min(1))
 print("iteration period ns: mean %.0f p50 %.0f" % (per.mean(), np.median(per)))
 slow = np.argmax(work, axis=1)
 print("slowest block histogram (top):", np.bincount(slow, minlength=nb).argsort()[::-1][:8], np.sort(np.bincount(slow, minlength=nb))[::-1][:8])
+
+# per-stage latencies of thread 0's first task (where recorded)
+st = t[:, :, 3:7]
+ok = (st > 0).all(axis=2)
+if ok.any():
+    d = np.diff(st, axis=2)[ok] / 1.965
+    print("task stages ns (entry->record, record->dist, dist->candidates): mean",
+          d.mean(0).round(0), "p90", np.percentile(d, 90, axis=0).round(0))
+    loop = (t[:, :, 7] - t[:, :, 3])[ok] / 1.965
+    print("thread-0 task loop from first task entry ns: mean %.0f p90 %.0f" % (loop.mean(), np.percentile(loop, 90)))
+bp = t[:, :, 8:12]
+okb = (bp > 0).all(axis=2)
+if okb.any():
+    d = np.diff(bp, axis=2)[okb] / 1.965
+    print("barrier3 ns (release fence, poll wait, slot reduce): mean", d.mean(0).round(0),
+          "p90", np.percentile(d, 90, axis=0).round(0))

@@ -15,6 +15,14 @@ import paper_1810_08218_b200 as g
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["v3", "v2"], autouse=True)
+def solver(request, monkeypatch):
+    """Run every parity test on both solver kernels: the queue-based kernel (v2,
+    default) and the claimer-first kernel with BFS-ordered packed records (v3)."""
+    monkeypatch.setenv("GEODIST_SOLVER", request.param[1])
+    return request.param
+
+
 def mesh_of(gd):
     return g.Mesh(gd["vertices"], gd["faces"])
 
