@@ -104,7 +104,9 @@ int geodist_device_count(int32_t* count);
 /* ---- meshes ---------------------------------------------------------- */
 /* Validates (validate_mesh, mesh.cpp:11-34), builds the rotational fans
  * (build_connectivity, connectivity.cpp:19-81) and uploads the fan-CSR to
- * `device`.  xyz: n*3 doubles, faces: nf*3 int32. */
+ * `device`.  xyz: n*3 doubles, faces: nf*3 int32.  xyz may be NULL for a
+ * topology-only mesh (toplesets / reorder only; compute_toplesets receives a
+ * Connectivity without positions). */
 int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int32_t nf,
                         int32_t device, geodist_mesh_t* out);
 int geodist_mesh_destroy(geodist_mesh_t mesh);
@@ -121,6 +123,16 @@ int geodist_mesh_fan(geodist_mesh_t mesh, int32_t v, int32_t* v1, int32_t* v2, i
  * (vertex v's ring r_0..r_d at cptr[v]+v); degree: n (or NULL). */
 int geodist_build_fans(const double* xyz, int32_t n, const int32_t* faces, int32_t nf,
                        int32_t* cptr, int32_t* ring, int32_t* degree);
+
+/* validate_mesh (mesh.cpp:11-34): GEODIST_EMESH with the reference's message. */
+int geodist_validate_mesh(const double* xyz, int32_t n, const int32_t* faces, int32_t nf);
+
+/* Host-only half-edge tables of build_connectivity (connectivity.cpp:19-81):
+ * twin[3*nf] (-1 on the boundary) and the fan-start half-edge per vertex
+ * (vertex_halfedge[n], -1 for isolated vertices); half-edge 3f+c runs from
+ * corner c to corner (c+1)%3 of face f.  xyz may be NULL (topology checks only). */
+int geodist_build_halfedges(const double* xyz, int32_t n, const int32_t* faces, int32_t nf,
+                            int32_t* twin, int32_t* vertex_halfedge);
 
 /* Host-side mesh generators (fixtures; bit-identical to mesh.cpp:36-105 for
  * grid and icosphere).  Sizes first, then fill caller arrays. */

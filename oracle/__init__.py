@@ -21,7 +21,7 @@ def build(quiet=True):
     """Compile the C restatement, and the reference when its sources exist."""
     targets = ["port"]
     if os.path.isdir("/root/reference/proj/src"):
-        targets.append("ref")
+        targets += ["ref", "acceptance"]
     out = subprocess.run(["make", "-C", HERE] + targets, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)

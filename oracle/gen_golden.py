@@ -117,7 +117,19 @@ def main():
         rec[f"degen_{prec[0]}"] = np.array(degs, bool)
     np.savez_compressed(os.path.join(OUT, "planar_update.npz"), **rec)
     print("planar_update", cnt)
+    acceptance()
+
+
+def acceptance():
+    """Reference acceptance-suite output (timings stripped): oracle/_ref/acceptance_ref."""
+    import re
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "acceptance_ref")
+    out = subprocess.run([exe], capture_output=True, text=True).stdout
+    text = "".join(re.sub(r" \[[0-9.]+s\]$", "", ln) + "\n" for ln in out.splitlines())
+    open(os.path.join(OUT, "acceptance_reference.txt"), "w").write(text)
 
 
 if __name__ == "__main__":
     main()
+

@@ -18,7 +18,7 @@ GEODIST_OK, GEODIST_EINVAL, GEODIST_EMESH, GEODIST_ECUDA, GEODIST_ENOMEM = range
 EXPORTED = [
     "geodist_last_error", "geodist_version", "geodist_device_count", "geodist_mesh_create",
     "geodist_mesh_destroy", "geodist_mesh_sizes", "geodist_mesh_degrees", "geodist_mesh_fan",
-    "geodist_build_fans", "geodist_grid_sizes", "geodist_generate_grid", "geodist_icosphere_sizes",
+    "geodist_build_fans", "geodist_validate_mesh", "geodist_build_halfedges", "geodist_grid_sizes", "geodist_generate_grid", "geodist_icosphere_sizes",
     "geodist_generate_icosphere", "geodist_perturb_radial", "geodist_torus_sizes",
     "geodist_generate_torus", "geodist_heightfield", "geodist_toplesets",
     "geodist_reorder_for_bands", "geodist_ptp", "geodist_ptp_ordered", "geodist_voronoi",
@@ -80,6 +80,8 @@ def lib():
         L.geodist_mesh_fan.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.c_int32,
                                        C.POINTER(C.c_int32)]
         L.geodist_build_fans.argtypes = [_f64p, C.c_int32, _i32p, C.c_int32, _i32p, _i32p, _vp]
+        L.geodist_validate_mesh.argtypes = [_f64p, C.c_int32, _i32p, C.c_int32]
+        L.geodist_build_halfedges.argtypes = [_vp, C.c_int32, _i32p, C.c_int32, _i32p, _i32p]
         L.geodist_grid_sizes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                          C.POINTER(C.c_int32)]
         L.geodist_generate_grid.argtypes = [C.c_int32, C.c_int32, C.c_double, _f64p, _i32p]

@@ -246,7 +246,11 @@ struct geodist_mesh_s {
         if (stream) cudaStreamDestroy(stream);
     }
 
+    bool has_geometry = true;
+
     void ensure_prec(int p) {
+        if (!has_geometry)
+            throw Fail(GEODIST_EINVAL, "mesh was created without vertex positions (topology only)");
         PrecTables& t = prec[p];
         if (t.quad) return;
         const size_t ring_len = static_cast<size_t>(corners) + n;
@@ -526,7 +530,7 @@ int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int3
     return guarded([&] {
         if (!out) throw Fail(GEODIST_EINVAL, "null output handle");
         *out = nullptr;
-        if (n < 0 || nf < 0 || (n > 0 && !xyz) || (nf > 0 && !faces))
+        if (n < 0 || nf < 0 || (nf > 0 && !faces))
             throw Fail(GEODIST_EINVAL, "invalid mesh arrays");
         Fans fans = build_fans(xyz, n, faces, nf);  // runtime_error -> EMESH
         if (n > kIdMask) throw Fail(GEODIST_EINVAL, "mesh too large: at most 2^27-1 vertices");
@@ -543,7 +547,10 @@ int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int3
         m->faces = dalloc<int>(3 * static_cast<size_t>(nf));
         m->cptr = dalloc<int>(static_cast<size_t>(n) + 1);
         m->ring = dalloc<int>(fans.ring.size());
-        cuda_ok(cudaMemcpy(m->xyz, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice), "upload");
+        m->has_geometry = xyz != nullptr;
+        if (xyz)
+            cuda_ok(cudaMemcpy(m->xyz, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice),
+                    "upload");
         if (nf)
             cuda_ok(cudaMemcpy(m->faces, faces, sizeof(int) * 3 * nf, cudaMemcpyHostToDevice),
                     "upload");
@@ -598,6 +605,19 @@ int geodist_build_fans(const double* xyz, int32_t n, const int32_t* faces, int32
         std::copy(f.cptr.begin(), f.cptr.end(), cptr);
         std::copy(f.ring.begin(), f.ring.end(), ring);
         if (degree) std::copy(f.degree.begin(), f.degree.end(), degree);
+    });
+}
+
+int geodist_validate_mesh(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) {
+    return guarded([&] { validate(xyz, n, faces, nf); });
+}
+
+int geodist_build_halfedges(const double* xyz, int32_t n, const int32_t* faces, int32_t nf,
+                            int32_t* twin, int32_t* vertex_halfedge) {
+    return guarded([&] {
+        const Fans f = build_fans(xyz, n, faces, nf);
+        std::copy(f.twin.begin(), f.twin.end(), twin);
+        std::copy(f.vstart.begin(), f.vstart.end(), vertex_halfedge);
     });
 }
 

@@ -27,7 +27,7 @@
 namespace gdb {
 
 void validate(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) {
-    for (int32_t v = 0; v < n; ++v) {
+    for (int32_t v = 0; xyz != nullptr && v < n; ++v) {
         const double* p = xyz + 3 * static_cast<size_t>(v);
         if (!std::isfinite(p[0]) || !std::isfinite(p[1]) || !std::isfinite(p[2]))
             throw std::runtime_error("vertex " + std::to_string(v) + " has non-finite coordinates");
@@ -41,7 +41,7 @@ void validate(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) {
                                          std::to_string(n) + " vertices)");
         if (t[0] == t[1] || t[1] == t[2] || t[0] == t[2])
             throw std::runtime_error("face " + std::to_string(f) + " repeats a vertex index");
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; xyz != nullptr && c < 3; ++c) {
             const int32_t a = t[c], b = t[(c + 1) % 3];
             const double* pa = xyz + 3 * static_cast<size_t>(a);
             const double* pb = xyz + 3 * static_cast<size_t>(b);
@@ -98,7 +98,7 @@ Fans build_fans(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) 
     F.ring.clear();
     F.ring.reserve(static_cast<size_t>(nhe) + n);
     F.degree.assign(static_cast<size_t>(n), 0);
-    std::vector<int32_t> c_v1, c_v2;
+    F.vstart.assign(static_cast<size_t>(n), -1);
     int32_t corners = 0;
     for (int32_t v = 0; v < n; ++v) {
         F.cptr[v] = corners;
@@ -115,6 +115,7 @@ Fans build_fans(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) 
             h = nxt(twin[h]);
             if (h == h0) break;
         }
+        F.vstart[v] = h;
         // Walk h -> twin(prev(h)) (connectivity.hpp:35-44).
         int32_t w = h, last = h, count = 0;
         do {
@@ -134,6 +135,7 @@ Fans build_fans(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) 
         corners += count;
     }
     F.cptr[n] = corners;
+    F.twin = std::move(twin);
     return F;
 }
 

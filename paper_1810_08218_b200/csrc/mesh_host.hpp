@@ -12,6 +12,8 @@ struct Fans {
     std::vector<int32_t> cptr;    // n+1 corner offsets
     std::vector<int32_t> ring;    // cptr[n] + n entries; vertex v at cptr[v] + v
     std::vector<int32_t> degree;  // graph degree (Connectivity::degree)
+    std::vector<int32_t> twin;    // half-edge twins (3 nf), -1 on the boundary
+    std::vector<int32_t> vstart;  // fan-start half-edge per vertex, -1 if isolated
     int32_t ring_offset(int32_t v) const { return cptr[v] + v; }
 };
 
