@@ -159,6 +159,8 @@ struct Workspace {
         blists = dalloc<int>(2 * static_cast<size_t>(blocks) * claim_cap);
     }
     void fill(RunArgs& a) const {
+        const char* w = getenv("GEODIST_WIDE");
+        a.wide_factor = w ? atoi(w) : kWideFactor;
         a.dist0 = dist0;
         a.dist1 = dist1;
         a.lab0 = lab0;

@@ -31,6 +31,8 @@ constexpr int kMetaShift = 27;     // entry 0 bits 27..30 hold the corner count 
 constexpr int kIdMask = (1 << kMetaShift) - 1;
 constexpr int kEllOverflow = 15;   // d code: more than 7 corners, use the CSR tables
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWideFactor = 2;     // thread-per-vertex once the band exceeds 2x the CTA groups
+                                   // (RunArgs.wide_factor; GEODIST_WIDE overrides)
 constexpr int kSlotsPerLane = 8;       // v3: barrier payload slots read per lane of warp 0
 constexpr int kMaxGroupBlocks = 32 * kSlotsPerLane;  // v3: CTAs per query group
 
@@ -128,6 +130,7 @@ struct RunArgs {
     void* pL;            // 8 T per position
     void* pquad;         // 8 Quad<T> per position
     unsigned long long* blk_slot;  // [2][gridDim.x][2]: max-rel bits, claim count
+    int wide_factor;     // v2: band > wide_factor * CTA groups -> one thread per vertex
     int* blists;         // [2][gridDim.x][claim_cap] per-CTA claim lists
     int claim_cap;       // capacity of one claim list
 };

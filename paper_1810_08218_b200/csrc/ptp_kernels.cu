@@ -369,6 +369,11 @@ __device__ __forceinline__ void append_claims(bool claim, int id, int* tail, int
     }
 }
 
+// One claim appended with its own atomic (overflow vertices only).
+__device__ __forceinline__ void append_one(int id, int* tail, int* queue) {
+    queue[atomicAdd(tail, 1)] = id;
+}
+
 // Candidates of the corners one lane holds in a chunk.  Lane gl holds ring
 // entries gl and gl+4 of the chunk; corner c = (entry c, entry c+1), so
 //   corner gl   pairs (gl, gl+1): entry gl+1 is lane gl+1's first entry, except
@@ -552,6 +557,178 @@ __device__ __forceinline__ void relax_group(const MeshDev& M, bool act, int p, i
         }
     }
     if (act && gl == 0) {
+        dc[v] = best;
+        if (LABELS) lc[v] = blab;
+        calls += d;
+        const T rc = rel_change(tv, best);
+        if (p < fe && rc > my_max) my_max = rc;
+        if (last_change != nullptr && rc >= eps) last_change[v] = kk;
+    }
+}
+
+// ELL row of one vertex in registers, entries de-interleaved (entry e at slot
+// (e % 4) * 2 + e / 4).
+template <typename T> struct RowL;
+template <> struct RowL<float> {
+    __device__ __forceinline__ static void load(const void* base, size_t v, float* L) {
+        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + v * kEllW);
+        const float4 a = __ldg(p), b = __ldg(p + 1);
+        L[0] = a.x; L[4] = a.y; L[1] = a.z; L[5] = a.w;
+        L[2] = b.x; L[6] = b.y; L[3] = b.z; L[7] = b.w;
+    }
+};
+template <> struct RowL<double> {
+    __device__ __forceinline__ static void load(const void* base, size_t v, double* L) {
+        const double2* p =
+            reinterpret_cast<const double2*>(static_cast<const double*>(base) + v * kEllW);
+        const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
+        L[0] = a.x; L[4] = a.y; L[1] = b.x; L[5] = b.y;
+        L[2] = c.x; L[6] = c.y; L[3] = d.x; L[7] = d.y;
+    }
+};
+
+// Warp-aggregated append of up to kEllW claims per lane (one global atomic per warp).
+__device__ __forceinline__ void append_claims_multi(const bool* claim, const int* id, int* tail,
+                                                    int* queue) {
+    int mine = 0;
+#pragma unroll
+    for (int e = 0; e < kEllW; ++e) mine += claim[e] ? 1 : 0;
+    const int l32 = threadIdx.x & 31;
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (l32 >= o) incl += y;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    if (total == 0) return;
+    int base = 0;
+    if (l32 == 31) base = atomicAdd(tail, total);
+    base = __shfl_sync(kFull, base, 31) + incl - mine;
+#pragma unroll
+    for (int e = 0; e < kEllW; ++e)
+        if (claim[e]) queue[base++] = id[e];
+}
+
+// Relax one band vertex per THREAD (wide bands): relax_vertex's sequential fan
+// scan with strict '<' (update_kernel.hpp:93-120) -- 32 vertices advance per warp
+// instruction instead of 8, no shuffles.  All lanes call it (claims are
+// warp-aggregated); `act` predicates the lane.
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax_thread(const MeshDev& M, bool act, int p, int kk,
+                                             const int* queue, const T* dp, T* dc,
+                                             const int* lp, int* lc, int fe, bool expand,
+                                             int* level, int* queue_w, int* tail_ptr, T eps,
+                                             int* last_change, T& my_max, long long& calls,
+                                             long long& degs) {
+    const T inf = Lim<T>::inf();
+    int v = 0, d = 0;
+    int raw[kEllW];
+    T L[kEllW];
+#pragma unroll
+    for (int e = 0; e < kEllW; ++e) {
+        raw[e] = 0;
+        L[e] = T(0);
+    }
+    if (act) {
+        v = ldcg(queue + p);
+        const int4* rp = reinterpret_cast<const int4*>(M.ering) + 2 * static_cast<size_t>(v);
+        const int4 a = __ldg(rp), b = __ldg(rp + 1);
+        raw[0] = a.x; raw[4] = a.y; raw[1] = a.z; raw[5] = a.w;
+        raw[2] = b.x; raw[6] = b.y; raw[3] = b.z; raw[7] = b.w;
+        RowL<T>::load(M.eL, v, L);
+        d = (raw[0] >> kMetaShift) & 15;
+    }
+    const bool ovf = act && d == kEllOverflow;
+    int id[kEllW];
+    bool claim[kEllW];
+#pragma unroll
+    for (int e = 0; e < kEllW; ++e) {
+        id[e] = raw[e] & kIdMask;
+        claim[e] = false;
+    }
+    T tv = inf;
+    int lv = -1;
+    T best = inf;
+    int blab = -1;
+    if (act) {
+        tv = ldcg(dp + v);
+        if (LABELS) lv = ldcg(lp + v);
+        best = tv;
+        blab = lv;
+    }
+    if (act && !ovf && d > 0) {
+        T t[kEllW];
+        int l[kEllW];
+#pragma unroll
+        for (int e = 0; e < kEllW; ++e) {
+            t[e] = inf;
+            l[e] = -1;
+            if (e <= d) {
+                if (expand) claim[e] = atomicCAS(level + id[e], -1, kk + 1) == -1;
+                t[e] = ldcg(dp + id[e]);
+                if (LABELS) l[e] = ldcg(lp + id[e]);
+            }
+        }
+        const size_t qb = static_cast<size_t>(v) * kEllW;
+#pragma unroll
+        for (int c = 0; c < kEllW - 1; ++c) {
+            if (c < d) {
+                Quad<T> q;
+                q.load(M.equad, static_cast<int>(qb + ell_slot(c)));
+                const bool mixed = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
+                int side, deg;
+                const T val = corner_candidate(t[c], t[c + 1], L[c], L[c + 1], q.q11, q.q12,
+                                               q.q22, q.a, raw[c] < 0, mixed, side, deg);
+                degs += deg;
+                if (val < best) {
+                    best = val;
+                    if (LABELS) blab = side == 0 ? l[c] : l[c + 1];
+                }
+            }
+        }
+    } else if (ovf) {
+        // more than 7 corners: CSR tables, sequential fan walk
+        const int c0 = __ldg(M.cptr + v);
+        d = __ldg(M.cptr + v + 1) - c0;
+        const int r0 = c0 + v;
+        const T* ringL = static_cast<const T*>(M.ringL);
+        int x0 = __ldg(M.ring + r0);
+        int i0 = x0 & INT_MAX;
+        T t0 = ldcg(dp + i0), L0 = __ldg(ringL + r0);
+        int l0 = LABELS ? ldcg(lp + i0) : -1;
+        if (expand && atomicCAS(level + i0, -1, kk + 1) == -1) {
+            prefetch_ell<T>(M, i0);
+            append_one(i0, tail_ptr, queue_w);
+        }
+        for (int c = 0; c < d; ++c) {
+            const int x1 = __ldg(M.ring + r0 + c + 1);
+            const int i1 = x1 & INT_MAX;
+            const T t1 = ldcg(dp + i1), L1 = __ldg(ringL + r0 + c + 1);
+            const int l1 = LABELS ? ldcg(lp + i1) : -1;
+            if (expand && atomicCAS(level + i1, -1, kk + 1) == -1) {
+                prefetch_ell<T>(M, i1);
+                append_one(i1, tail_ptr, queue_w);
+            }
+            Quad<T> q;
+            q.load(M.quad, c0 + c);
+            const bool mixed = LABELS && l0 != l1 && t0 != inf && t1 != inf;
+            int side, deg;
+            const T val = corner_candidate(t0, t1, L0, L1, q.q11, q.q12, q.q22, q.a, x0 < 0, mixed,
+                                           side, deg);
+            degs += deg;
+            if (val < best) {
+                best = val;
+                if (LABELS) blab = side == 0 ? l0 : l1;
+            }
+            x0 = x1; i0 = i1; t0 = t1; L0 = L1; l0 = l1;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < kEllW; ++e)
+        if (claim[e]) prefetch_ell<T>(M, id[e]);
+    append_claims_multi(claim, id, tail_ptr, queue_w);
+    if (act) {
         dc[v] = best;
         if (LABELS) lc[v] = blab;
         calls += d;
@@ -752,15 +929,27 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run_kernel(RunArgs A) {
                 dcur[v] = ldcg(dp + v);
                 if (LABELS) lc[v] = ldcg(lp + v);
             }
-            // relax the band [bb, be)   (ptp.cpp:96-110)
+            // relax the band [bb, be)   (ptp.cpp:96-110): 4 lanes per vertex while the
+            // band fits the CTA groups (latency), one thread per vertex beyond (throughput)
             my_max = T(0);
-            for (int t = first_task;; t += stride) {
-                const bool act = t < ntask;
-                if (!__any_sync(kFull, act)) break;
-                const int p = bb_ + t;
-                relax_group<T, LABELS>(M, act, p, kk, queue, dp, dcur, lp, lc, fe_,
-                                       p >= expb && p < expe, level, queue, &ctl->tail, eps,
-                                       A.last_change, my_max, calls, degs);
+            if (ntask <= A.wide_factor * stride) {
+                for (int t = first_task;; t += stride) {
+                    const bool act = t < ntask;
+                    if (!__any_sync(kFull, act)) break;
+                    const int p = bb_ + t;
+                    relax_group<T, LABELS>(M, act, p, kk, queue, dp, dcur, lp, lc, fe_,
+                                           p >= expb && p < expe, level, queue, &ctl->tail, eps,
+                                           A.last_change, my_max, calls, degs);
+                }
+            } else {
+                for (int t = gtid;; t += gthreads) {
+                    const bool act = t < ntask;
+                    if (!__any_sync(kFull, act)) break;
+                    const int p = bb_ + t;
+                    relax_thread<T, LABELS>(M, act, p, kk, queue, dp, dcur, lp, lc, fe_,
+                                            p >= expb && p < expe, level, queue, &ctl->tail, eps,
+                                            A.last_change, my_max, calls, degs);
+                }
             }
             const T bmax = block_max(my_max, red_t);
             if (dbg) dslot[1] = gtimer();

@@ -15,11 +15,16 @@ import paper_1810_08218_b200 as g
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["v3", "v2"], autouse=True)
+@pytest.fixture(params=["v3", "v2", "v2-wide"], autouse=True)
 def solver(request, monkeypatch):
-    """Run every parity test on both solver kernels: the queue-based kernel (v2,
-    default) and the claimer-first kernel with BFS-ordered packed records (v3)."""
+    """Run every parity test on all solver paths: the queue-based kernel (v2, default),
+    the same kernel forced onto its thread-per-vertex wide-band path (v2-wide), and the
+    claimer-first kernel with BFS-ordered packed records (v3)."""
     monkeypatch.setenv("GEODIST_SOLVER", request.param[1])
+    if request.param == "v2-wide":
+        monkeypatch.setenv("GEODIST_WIDE", "0")
+    else:
+        monkeypatch.delenv("GEODIST_WIDE", raising=False)
     return request.param
 
 
