@@ -324,7 +324,8 @@ void check_config(const geodist_ptp_config* c) {
 // overflow).  Tests run both.
 int solver_version() {
     const char* e = getenv("GEODIST_SOLVER");
-    return (e && e[0] == '3') ? 3 : 2;
+    if (e && (e[0] == '3' || e[0] == '4')) return e[0] - '0';
+    return 2;
 }
 
 // Everything one distance-field solve needs from the caller.
@@ -458,7 +459,7 @@ void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
     }
     QueryStats qs{};
     cuda_ok(cudaMemcpy(&qs, a.qstats, sizeof(QueryStats), cudaMemcpyDeviceToHost), "stats");
-    if (qs.pad == 2 && version == 3) {
+    if (qs.pad >= 2 && version >= 3) {
         // a CTA claimed more vertices in one iteration than its shared-memory
         // list holds: redo the field with the general kernel
         run_solve(mh, q, 2);
@@ -884,8 +885,8 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         cuda_ok(cudaMemcpy(hs.data(), d_samples, sizeof(int) * count, cudaMemcpyDeviceToHost), "d2h");
         cuda_ok(cudaMemcpy(hh.data(), hist.get(), sizeof(QueryStats) * count,
                            cudaMemcpyDeviceToHost), "d2h");
-        if (version == 3 && std::any_of(hh.begin(), hh.end(),
-                                        [](const QueryStats& x) { return x.pad == 2; })) {
+        if (version >= 3 && std::any_of(hh.begin(), hh.end(),
+                                        [](const QueryStats& x) { return x.pad >= 2; })) {
             version = 2;  // claim-list overflow: redo the sampling on the general kernel
             goto fps_retry;
         }
@@ -976,8 +977,8 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         cuda_ok(cudaMemcpyAsync(hq.data(), qs.get(), sizeof(QueryStats) * nq,
                                 cudaMemcpyDeviceToHost, st), "d2h");
         cuda_ok(cudaStreamSynchronize(st), "batch");
-        if (version == 3 &&
-            std::any_of(hq.begin(), hq.end(), [](const QueryStats& x) { return x.pad == 2; })) {
+        if (version >= 3 &&
+            std::any_of(hq.begin(), hq.end(), [](const QueryStats& x) { return x.pad >= 2; })) {
             version = 2;
             goto batch_retry;
         }

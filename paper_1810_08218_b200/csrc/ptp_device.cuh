@@ -55,6 +55,10 @@ struct alignas(128) GroupCtl {
     int s_tail, s_limk, s_bb, s_fe, s_frzb, s_frze, pad3[2];
     unsigned long long relax, degen, updates;
     unsigned long long pad4[5];
+    // v4 barrier words (ring of 4): bits 0-15 arrivals, 16-31 CTAs with a front
+    // change >= eps, 32-63 claims made in the iteration
+    unsigned long long barw[4];
+    unsigned long long pad5[12];
     // FPS / argmax scratch: per-CTA (value bits, index)
 };
 
@@ -133,6 +137,7 @@ struct RunArgs {
     int wide_factor;     // v2: band > wide_factor * CTA groups -> one thread per vertex
     int* blists;         // [2][gridDim.x][claim_cap] per-CTA claim lists
     int claim_cap;       // capacity of one claim list
+    int cache_slots;     // v4: shared-memory record cache slots per CTA
 };
 
 // Per-CTA barrier payload slot (16 B): max relative change bits and claims.

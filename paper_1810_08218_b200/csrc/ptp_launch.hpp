@@ -22,6 +22,9 @@ void launch_planar_test(int precision, const double* x1, const double* x2, const
 // version 3: claimer-first solver (default); version 2: general queue-based solver
 // (used when a CTA's claims overflow its shared-memory list).
 int run_max_blocks(int precision, bool labels, int device, int version = 3);
+// v4 (ptp_run4.cu): record-cache bytes (dynamic shared memory) and kernel entry
+size_t run4_dyn_smem(int precision, bool labels);
+const void* run4_kernel_ptr(int precision, bool labels);
 cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st,
                        int version = 3);
 

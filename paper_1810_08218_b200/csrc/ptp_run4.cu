@@ -1,0 +1,872 @@
+// v4 PTP solver (sm_100a): stable position ownership, on-chip record cache,
+// payload-carrying grid barrier.
+//
+// Same semantics as ptp_run_kernel / ptp_run3_kernel (the band loop of
+// run_impl<T>, reference src/ptp.cpp:79-132, with compute_toplesets'
+// BFS, src/toplesets.cpp:37-55, fused in) and the same arithmetic
+// (corner_candidate / chunk_candidates), so results are bit-identical.  What
+// changes is where every dependent memory trip of an iteration goes:
+//
+//  * BFS position p of a query is owned by CTA p % nb for the whole solve.  A
+//    vertex's packed record (id, ELL ring, |x|, Gram quads -- the
+//    reorder_for_bands layout, toplesets.cpp:60-89) is written once at its
+//    position by the CTA that claims it, read from L2 by the owner at the
+//    vertex's first relaxation and kept in the owner's shared memory for every
+//    later iteration (a ring of R slots, slot p / nb).  An old band vertex
+//    therefore costs one L2 trip per iteration: the neighbour distances.
+//  * claims get their BFS position immediately (warp-aggregated atomicAdd on
+//    the queue tail) and the claimer copies the claimed vertex's ELL row into
+//    the packed record at that position while the candidates are computed.
+//  * the grid barrier is one red.release.add of a 64-bit word per CTA whose
+//    fields carry the iteration's payload: bits 0-15 arrivals, 16-31 CTAs with
+//    a front change >= eps (ptp.cpp:107,114), 32-63 claims (the next
+//    topleset's size).  Polling that word is the only trip after the barrier:
+//    topleset limits live in a shared-memory ring, not in global memory.
+#include "ptp_common.cuh"
+#include "ptp_launch.hpp"
+
+namespace gdb {
+
+namespace {
+
+constexpr int kLimRing = 1024;  // topleset limits kept on chip (levels)
+
+struct Bcast4 {
+    int k, i, j, bb, oe, be, fe, frzb, frze, parity, done, expand;
+    // this CTA's share (positions p == lb mod nb): band tasks p0 + t * nb below
+    // be (record-cache slot a0 + t), frozen positions f0 + t * nb for t < nfz
+    int p0, a0, f0, fa0, nfz;
+};
+
+constexpr int kCacheSlots = 512;  // record-cache ring (power of two) per CTA
+
+__device__ __forceinline__ void red_release_u64(unsigned long long* p, unsigned long long x) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long atom_release_add_u64(unsigned long long* p,
+                                                                   unsigned long long x) {
+    unsigned long long r;
+    asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(x) : "memory");
+    return r;
+}
+__device__ __forceinline__ int ld_relaxed_i32(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long x) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+
+// Shared-memory record cache: one lane's share (entries gl and gl+4) of slot s
+// lives at index s * 4 + gl of each array.
+template <typename T> struct Cache {
+    int2* rr;    // ring entries (ids | flags; entry 0 carries the corner count)
+    int2* pv;    // (position tag, vertex id)
+    T* L;        // |x| of the two entries
+    Quad<T>* q;  // Gram quads of corners gl and gl+4
+    static constexpr size_t bytes_per_slot() {
+        return 4 * (sizeof(int2) + sizeof(int2) + 2 * sizeof(T) + 2 * sizeof(Quad<T>));
+    }
+    __device__ void bind(unsigned char* base, int R) {
+        rr = reinterpret_cast<int2*>(base);
+        pv = rr + 4 * R;
+        L = reinterpret_cast<T*>(pv + 4 * R);
+        q = reinterpret_cast<Quad<T>*>(L + 8 * R);
+    }
+};
+
+template <typename T> __device__ __forceinline__ void sm_store_quad(Quad<T>* at, const Quad<T>& x);
+template <typename T> __device__ __forceinline__ void sm_load_quad(const Quad<T>* at, Quad<T>& x);
+template <> __device__ __forceinline__ void sm_store_quad<float>(Quad<float>* at, const Quad<float>& x) {
+    *reinterpret_cast<float4*>(at) = make_float4(x.q11, x.q12, x.q22, x.a);
+}
+template <> __device__ __forceinline__ void sm_load_quad<float>(const Quad<float>* at, Quad<float>& x) {
+    const float4 v = *reinterpret_cast<const float4*>(at);
+    x.q11 = v.x; x.q12 = v.y; x.q22 = v.z; x.a = v.w;
+}
+template <> __device__ __forceinline__ void sm_store_quad<double>(Quad<double>* at, const Quad<double>& x) {
+    double2* p = reinterpret_cast<double2*>(at);
+    p[0] = make_double2(x.q11, x.q12);
+    p[1] = make_double2(x.q22, x.a);
+}
+template <> __device__ __forceinline__ void sm_load_quad<double>(const Quad<double>* at, Quad<double>& x) {
+    const double2* p = reinterpret_cast<const double2*>(at);
+    const double2 u = p[0], w = p[1];
+    x.q11 = u.x; x.q12 = u.y; x.q22 = w.x; x.a = w.y;
+}
+
+// Claims of one warp go to the CTA's claim list (index from a shared-memory
+// counter; entries beyond kSmemClaims spill to the CTA's global list).  Their
+// BFS positions are assigned at the grid barrier: the arrival atomic returns
+// the claims of the CTAs that arrived earlier, and warp 0 writes the list to
+// pv[level start + that prefix + index] (claim_list_flush).  The claimer also
+// pulls the vertex's ELL row towards L2 for the owner's first relaxation.
+constexpr int kSmemClaims = 2048;
+
+template <typename T>
+__device__ __forceinline__ void claim_records(bool ca, int ia, bool cb, int ib,
+                                              const MeshDev& M, int* s_list, int* g_list,
+                                              int g_cap, int* s_ccnt, int* err) {
+    const unsigned ba = __ballot_sync(kFull, ca), bbal = __ballot_sync(kFull, cb);
+    const int na = __popc(ba);
+    const int total = na + __popc(bbal);
+    if (total == 0) return;
+    if (ca) prefetch_ell<T>(M, ia);
+    if (cb) prefetch_ell<T>(M, ib);
+    const int l32 = threadIdx.x & 31;
+    int base = 0;
+    if (l32 == 0) base = atomicAdd(s_ccnt, total);
+    base = __shfl_sync(kFull, base, 0);
+    const unsigned lt = (1u << l32) - 1u;
+    auto put = [&](int at, int id) {
+        if (at < kSmemClaims) s_list[at] = id;
+        else if (at - kSmemClaims < g_cap) g_list[at - kSmemClaims] = id;
+        else *err = 2;
+    };
+    if (ca) put(base + __popc(ba & lt), ia);
+    if (cb) put(base + na + __popc(bbal & lt), ib);
+}
+
+struct ClaimCtx {
+    int* s_list;
+    int* g_list;
+    int g_cap;
+    int* ccnt;
+    int* err;
+};
+
+// Relax the vertex at BFS position p (4-lane group; relax_vertex,
+// update_kernel.hpp:93-120).  Lanes return their claims in (ca, ia, cb, ib).
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
+                                       int sl, bool act, bool is_new, bool cached, int p,
+                                       int kk, const int* pv, const int* pring, const T* pL,
+                                       const char* pquad, const T* dp, T* dc, const int* lp,
+                                       int* lc, int fe, bool expand, int* level, T eps,
+                                       const ClaimCtx& CC, int& nonconv, T& my_max,
+                                       long long& calls, long long& degs, bool& ca_claim,
+                                       int& ida, bool& cb_claim, int& idb,
+                                       unsigned long long* tdbg) {
+    const T inf = Lim<T>::inf();
+    if (tdbg) tdbg[3] = cyc();
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int g0 = (threadIdx.x & 31) & ~(kGroup - 1);
+    int v = 0;
+    int2 rr = make_int2(0, 0);
+    T La = T(0), Lb = T(0);
+    Quad<T> qa, qb;
+    qa.q11 = qa.q12 = qa.q22 = qa.a = T(0);
+    qb = qa;
+    const int ci = sl * 4 + gl;
+    bool hit = false;
+    if (act && cached && !is_new) {
+        const int2 tg = C.pv[ci];
+        if (tg.x == p) {
+            hit = true;
+            v = tg.y;
+            rr = C.rr[ci];
+            La = C.L[2 * ci];
+            Lb = C.L[2 * ci + 1];
+            sm_load_quad<T>(C.q + 2 * ci, qa);
+            sm_load_quad<T>(C.q + 2 * ci + 1, qb);
+        }
+    }
+    if (act && !hit) {
+        const size_t pb = static_cast<size_t>(p) * kEllW;
+        if (is_new) {
+            // the claimer's warp 0 writes pv[p] right after its barrier arrival
+            v = ld_relaxed_i32(pv + p);
+            for (int spin = 0; v < 0; ++spin) {
+                if (spin > (1 << 22)) {
+                    *CC.err = 3;
+                    v = 0;
+                    break;
+                }
+                v = ld_relaxed_i32(pv + p);
+            }
+        } else {
+            v = ldcg(pv + p);
+        }
+        if (is_new) {
+            // first relaxation: the id-indexed ELL row (pulled into L2 by the
+            // claimer), committed to the packed record at the position
+            const size_t eb = static_cast<size_t>(v) * kEllW;
+            rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
+            Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
+            qa.load(M.equad, static_cast<int>(eb + 2 * gl));
+            qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
+            reinterpret_cast<int2*>(const_cast<int*>(pring))[(pb >> 1) + gl] = rr;
+            Ell2<T>::store(const_cast<T*>(pL), pb + 2 * gl, La, Lb);
+            qa.store_at(const_cast<char*>(pquad), pb + 2 * gl);
+            qb.store_at(const_cast<char*>(pquad), pb + 2 * gl + 1);
+        } else {
+            rr = __ldcg(reinterpret_cast<const int2*>(pring) + (pb >> 1) + gl);
+            Ell2<T>::load_cg(pL, pb + 2 * gl, La, Lb);
+            qa.load_cg(pquad, pb + 2 * gl);
+            qb.load_cg(pquad, pb + 2 * gl + 1);
+        }
+        if (cached) {
+            C.pv[ci] = make_int2(p, v);
+            C.rr[ci] = rr;
+            C.L[2 * ci] = La;
+            C.L[2 * ci + 1] = Lb;
+            sm_store_quad<T>(C.q + 2 * ci, qa);
+            sm_store_quad<T>(C.q + 2 * ci + 1, qb);
+        }
+    }
+    if (tdbg) tdbg[4] = gtimer_after(rr.x + v);
+    const int meta = __shfl_sync(kFull, rr.x, g0);
+    int d = act ? (meta >> kMetaShift) & 15 : 0;
+    const bool ovf = d == kEllOverflow;
+    ida = rr.x & kIdMask;
+    idb = rr.y & kIdMask;
+    const bool hasa = act && !ovf && d > 0 && gl <= d;
+    const bool hasb = act && !ovf && d > 0 && gl + kGroup <= d;
+    const bool exp = expand && is_new;
+    ca_claim = false;
+    cb_claim = false;
+    if (exp) {
+        if (hasa) ca_claim = atomicCAS(level + ida, -1, kk + 1) == -1;
+        if (hasb) cb_claim = atomicCAS(level + idb, -1, kk + 1) == -1;
+    }
+    T tv = inf;
+    int lv = -1;
+    if (act && gl == 0) {
+        tv = ldcg(dp + v);
+        if (LABELS) lv = ldcg(lp + v);
+    }
+    T ta = inf, tb = inf;
+    int la = -1, lb_ = -1;
+    if (hasa) {
+        ta = ldcg(dp + ida);
+        if (LABELS) la = ldcg(lp + ida);
+    }
+    if (hasb) {
+        tb = ldcg(dp + idb);
+        if (LABELS) lb_ = ldcg(lp + idb);
+    }
+    if (tdbg) tdbg[5] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv)));
+    T best = gl == 0 ? tv : inf;
+    int bidx = gl == 0 ? -1 : INT_MAX;
+    int blab = gl == 0 ? lv : -1;
+    chunk_candidates<T, LABELS>(gl, 0, ovf ? 0 : d, rr.x, rr.y, La, Lb, ta, tb, la, lb_, qa, qb,
+                                best, bidx, blab, degs);
+    if (tdbg) tdbg[6] = gtimer_after(__float_as_int(static_cast<float>(best)));
+
+    // overflow vertices (> 7 corners): CSR tables, 7 corners per chunk; their
+    // claims are appended one by one (rare: valence > 7)
+    if (__any_sync(kFull, act && ovf)) {
+        int c0 = 0;
+        if (act && ovf) {
+            c0 = __ldg(M.cptr + v);
+            d = __ldg(M.cptr + v + 1) - c0;
+        }
+        const int r0 = c0 + v;
+        int nch = act && ovf ? (d + kEllW - 2) / (kEllW - 1) : 0;
+        nch = __reduce_max_sync(kFull, nch);
+        const T* ringL = static_cast<const T*>(M.ringL);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int base = ch * (kEllW - 1);
+            const int ea = base + gl, ebb = base + gl + kGroup;
+            const bool ha = act && ovf && ea <= d, hb = act && ovf && ebb <= d;
+            int xa = 0, xb = 0;
+            T LA = T(0), LB = T(0), TA = inf, TB = inf;
+            int lA = -1, lB = -1;
+            Quad<T> QA, QB;
+            QA.q11 = QA.q12 = QA.q22 = QA.a = T(0);
+            QB = QA;
+            if (ha) {
+                xa = __ldg(M.ring + r0 + ea);
+                LA = __ldg(ringL + r0 + ea);
+                if (ea < d) QA.load(M.quad, c0 + ea);
+            }
+            if (hb) {
+                xb = __ldg(M.ring + r0 + ebb);
+                LB = __ldg(ringL + r0 + ebb);
+                if (ebb < d) QB.load(M.quad, c0 + ebb);
+            }
+            const int ia = xa & INT_MAX, ib = xb & INT_MAX;
+            bool cA = false, cB = false;
+            if (exp) {
+                if (ha) cA = atomicCAS(level + ia, -1, kk + 1) == -1;
+                if (hb) cB = atomicCAS(level + ib, -1, kk + 1) == -1;
+            }
+            if (ha) {
+                TA = ldcg(dp + ia);
+                if (LABELS) lA = ldcg(lp + ia);
+            }
+            if (hb) {
+                TB = ldcg(dp + ib);
+                if (LABELS) lB = ldcg(lp + ib);
+            }
+            const int dlim = act && ovf ? min(d, base + kEllW - 1) : 0;
+            chunk_candidates<T, LABELS>(gl, base, dlim, xa, xb, LA, LB, TA, TB, lA, lB, QA, QB,
+                                        best, bidx, blab, degs);
+            claim_records<T>(cA, ia, cB, ib, M, CC.s_list, CC.g_list, CC.g_cap, CC.ccnt,
+                             CC.err);
+        }
+    }
+
+    for (int o = kGroup / 2; o > 0; o >>= 1) {
+        const T ob = __shfl_xor_sync(kFull, best, o, kGroup);
+        const int oi = __shfl_xor_sync(kFull, bidx, o, kGroup);
+        int ol = -1;
+        if (LABELS) ol = __shfl_xor_sync(kFull, blab, o, kGroup);
+        if (ob < best || (ob == best && oi < bidx)) {
+            best = ob;
+            bidx = oi;
+            if (LABELS) blab = ol;
+        }
+    }
+    if (act && gl == 0) {
+        dc[v] = best;
+        if (LABELS) lc[v] = blab;
+        calls += d;
+        if (p < fe || A.last_change != nullptr) {
+            const T rc = rel_change(tv, best);
+            if (p < fe && rc >= eps) nonconv = 1;
+            if (p < fe && rc > my_max) my_max = rc;
+            if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
+        }
+    }
+}
+
+}  // namespace
+
+template <typename T, bool LABELS>
+__global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ Bcast4 S;
+    __shared__ int s_lim[kLimRing];
+    __shared__ int s_list[kSmemClaims];
+    __shared__ T red_t[kBlock / 32];
+    __shared__ long long red_l[kBlock / 32];
+    __shared__ double red_v[kBlock / 32];
+    __shared__ int red_i[kBlock / 32];
+    __shared__ int s_ccnt, s_err;
+    __shared__ unsigned long long s_bw;
+
+    const int tid = threadIdx.x;
+    constexpr int R = kCacheSlots;
+    Cache<T> C;
+    C.bind(dsm, R);
+    const int nb = A.blocks_per_group;
+    const int g = blockIdx.x / nb;
+    const int lb = blockIdx.x - g * nb;
+    GroupCtl* ctl = A.ctl + g;
+    const long long off = static_cast<long long>(g) * A.stride;
+    const long long off8 = off * kEllW;
+    T* dist[2] = {static_cast<T*>(A.dist0) + off, static_cast<T*>(A.dist1) + off};
+    int* lab[2] = {nullptr, nullptr};
+    if (LABELS) {
+        lab[0] = A.lab0 + off;
+        lab[1] = A.lab1 + off;
+    }
+    int* level = A.level + off;
+    int* pv = A.queue + off;
+    int* limits = A.limits + off;
+    int* pring = A.pring + off8;
+    T* pL = static_cast<T*>(A.pL) + off8;
+    char* pquad = static_cast<char*>(A.pquad) + off8 * sizeof(Quad<T>);
+    const MeshDev M = A.mesh;
+    const int n = M.n;
+    const T inf = Lim<T>::inf();
+    const T eps = static_cast<T>(A.eps);
+    const int gthreads = nb * kBlock;
+    const int gtid = lb * kBlock + tid;
+    unsigned long long* barw = ctl->barw;
+    int* g_list = A.blists + static_cast<size_t>(blockIdx.x) * A.claim_cap;
+    const ClaimCtx CC{s_list, g_list, A.claim_cap, &s_ccnt, &s_err};
+    unsigned bseq = 0;
+    const double inv_nb = 1.0 / nb;
+
+    // Grid barrier with payload; thread 0 runs post(word) before the CTA is
+    // released.  The arrival atomic returns the word as it was before this
+    // CTA's arrival: its claim field is the number of claims of the CTAs that
+    // arrived earlier, i.e. this CTA's offset inside the new topleset, and warp
+    // 0 writes the CTA's claim list to those positions.  Readers of the new
+    // positions (the owners, next iteration) wait for pv[p] >= 0.
+    auto barrier = [&](unsigned long long payload, int level_start, auto&& pre, auto&& post) {
+        __syncthreads();
+        if (tid < 32) {
+            unsigned long long* w = barw + (bseq & 3);
+            unsigned long long old = 0;
+            if (tid == 0) {
+                // word (bseq+2)&3 was last polled at barrier bseq-2; every CTA has
+                // arrived at bseq-1 since, so it is free until barrier bseq+2
+                if (lb == 0) st_relaxed_u64(barw + ((bseq + 2) & 3), 0ull);
+                old = atom_release_add_u64(w, payload + 1ull);
+                pre();  // overlaps the arrival's round trip
+            }
+            const int cnt = static_cast<int>(payload >> 32);
+            if (cnt > 0) {
+                const int at = level_start + static_cast<int>(__shfl_sync(kFull, old, 0) >> 32);
+                for (int x = tid; x < cnt; x += 32)
+                    pv[at + x] = x < kSmemClaims ? s_list[x] : g_list[x - kSmemClaims];
+            }
+            if (tid == 0) {
+                unsigned long long x;
+                do {
+                    x = ld_acquire_u64(w);
+                } while (static_cast<int>(x & 0xffffull) < nb);
+                post(x);
+            }
+        }
+        ++bseq;
+        __syncthreads();
+    };
+
+    // reset the record cache tags (smem does not survive launches)
+    for (int x = tid; x < 4 * R; x += kBlock) C.pv[x] = make_int2(-1, 0);
+
+    for (int q = g; q < A.nq; q += A.groups) {
+        const int s0 = A.src_off ? A.src_off[q] : 0;
+        const int m = A.src_off ? A.src_off[q + 1] - s0 : A.src_count;
+        const int* src = A.src + s0;
+        // thread-0 loop state (identical in every CTA of the group)
+        int k = 0, i = 1, rho = INT_MAX, parity = 0, bfs_open = 0, done = 0;
+        int tail = 0, limk = 0, bb = 0, fe = 0, frzb = 0, frze = 0;
+        int lim_top = -1;      // highest topleset limit index held in s_lim
+        bool use_glim = false; // limits read from global memory (ring too short)
+        unsigned long long upd = 0;
+        auto lim = [&](int r) -> int {
+            return (use_glim || r <= lim_top - kLimRing) ? ldcg(limits + r) : s_lim[r % kLimRing];
+        };
+        auto set_lim = [&](int r, int x) {
+            s_lim[r % kLimRing] = x;
+            if (r > lim_top) lim_top = r;
+        };
+        // this CTA's share of a position range: first owned position >= x and its
+        // cache slot (x / nb via a double reciprocal, corrected), and the count of
+        // owned positions in [x, y).  Thread 0 evaluates these while its barrier
+        // arrival is in flight, for both outcomes of the convergence test.
+        auto div_nb = [&](int x) {
+            int qq = static_cast<int>(static_cast<double>(x) * inv_nb);
+            if ((qq + 1) * nb <= x) ++qq;
+            if (qq * nb > x) --qq;
+            return qq;
+        };
+        auto first_owned = [&](int x, int& first, int& slot) {
+            const int qx = div_nb(x), r = x - qx * nb;
+            first = x + (lb >= r ? lb - r : lb - r + nb);
+            slot = qx + (lb >= r ? 0 : 1);
+        };
+        auto owned_count = [&](int first, int y) { return y > first ? div_nb(y - first + nb - 1) : 0; };
+        int sh_p0 = 0, sh_a0 = 0, sh_f0 = 0, sh_fa0 = 0, sh_nfz = 0;
+        auto shares_now = [&] {
+            first_owned(bb, sh_p0, sh_a0);
+            first_owned(frzb, sh_f0, sh_fa0);
+            sh_nfz = owned_count(sh_f0, frze);
+        };
+        int pf = -1;
+        auto publish = [&] {
+            S.done = done;
+            s_ccnt = 0;
+            if (done) return;
+            const int kk = k + 1;
+            const int j = bfs_open ? kk : min(kk, rho - 1);
+            S.k = kk;
+            S.i = i;
+            S.j = j;
+            S.bb = bb;
+            S.fe = fe;
+            const int be = (bfs_open || j + 1 == rho) ? tail : lim(j + 1);
+            S.be = be;
+            S.oe = bfs_open ? limk : be;  // newest topleset: records still in global memory
+            S.expand = bfs_open;
+            S.frzb = frzb;
+            S.frze = frze;
+            S.parity = parity;
+            pf = -1;
+            if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
+                pf = (bfs_open && i + 2 == kk + 1) ? tail : lim(i + 2);
+            if (A.trace != nullptr && lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
+            S.p0 = sh_p0;
+            S.a0 = sh_a0;
+            S.f0 = sh_f0;
+            S.fa0 = sh_fa0;
+            S.nfz = sh_nfz;
+        };
+
+        if (tid == 0) s_err = 0;
+        if (q != g)
+            for (int x = tid; x < 4 * R; x += kBlock) C.pv[x] = make_int2(-1, 0);
+        if (A.phase_init) {
+            // reset (ptp.cpp:61-68)
+            for (int v = gtid; v < n; v += gthreads) {
+                dist[0][v] = inf;
+                dist[1][v] = inf;
+                if (LABELS) {
+                    lab[0][v] = -1;
+                    lab[1][v] = -1;
+                }
+                if (A.fused_bfs) {
+                    level[v] = -1;
+                    pv[v] = -1;  // position not yet assigned (claim_records)
+                }
+                if (A.last_change) A.last_change[v] = 0;
+            }
+            if (gtid == 0) {
+                ctl->relax = ctl->degen = ctl->updates = 0;
+                ctl->slot[0] = ctl->slot[1] = ctl->slot[2] = 0ull;
+                ctl->err = 0;
+            }
+            barrier(0ull, 0, [] {}, [](unsigned long long) {});
+            // seed sources: d = 0, label = index in caller order (ptp.cpp:69-73)
+            for (int s = gtid; s < m; s += gthreads) {
+                const int v = src[s];
+                dist[0][v] = T(0);
+                dist[1][v] = T(0);
+                if (LABELS) {
+                    lab[0][v] = s;
+                    lab[1][v] = s;
+                }
+                if (A.fused_bfs) {
+                    level[v] = 0;
+                    pv[s] = v;
+                }
+            }
+            if (A.fused_bfs && gtid == 0) {
+                limits[0] = 0;
+                limits[1] = m;
+            }
+            if (!A.fused_bfs) {
+                // caller ordering: pack every reachable position's record up front
+                const int reach = ldcg(limits + A.given_rho);
+                for (long long x = gtid; x < static_cast<long long>(reach) * kEllW;
+                     x += gthreads) {
+                    const int p = static_cast<int>(x / kEllW), slot = static_cast<int>(x % kEllW);
+                    const int v = ldcg(pv + p);
+                    const size_t eb = static_cast<size_t>(v) * kEllW + slot;
+                    pring[x] = __ldg(M.ering + eb);
+                    pL[x] = __ldg(static_cast<const T*>(M.eL) + eb);
+                    Quad<T> qq;
+                    qq.load(M.equad, static_cast<int>(eb));
+                    qq.store_at(pquad, x);
+                }
+            }
+            if (tid == 0) s_ccnt = 0;
+            barrier(0ull, 0, [] {}, [](unsigned long long) {});
+            if (A.fused_bfs) {
+                // iteration 0: claim topleset 1 from the sources (ring walk only)
+                const int gl = tid & (kGroup - 1);
+                for (int t = lb + nb * (tid / kGroup);; t += nb * (kBlock / kGroup)) {
+                    const bool act = t < m;
+                    if (!__any_sync(kFull, act)) break;
+                    int v = 0, c0 = 0, d = 0;
+                    if (act) {
+                        v = ldcg(pv + t);
+                        c0 = __ldg(M.cptr + v);
+                        d = __ldg(M.cptr + v + 1) - c0;
+                    }
+                    int nch = d > 0 ? (d + 2 * kGroup) / (2 * kGroup) : 0;  // entries 0..d
+                    nch = __reduce_max_sync(kFull, nch);
+                    for (int ch = 0; ch < nch; ++ch) {
+                        const int ea = ch * 2 * kGroup + gl, eb2 = ea + kGroup;
+                        bool cA = false, cB = false;
+                        int ia = 0, ib = 0;
+                        if (act && d > 0 && ea <= d) {
+                            ia = __ldg(M.ring + c0 + v + ea) & INT_MAX;
+                            cA = atomicCAS(level + ia, -1, 1) == -1;
+                        }
+                        if (act && d > 0 && eb2 <= d) {
+                            ib = __ldg(M.ring + c0 + v + eb2) & INT_MAX;
+                            cB = atomicCAS(level + ib, -1, 1) == -1;
+                        }
+                        claim_records<T>(cA, ia, cB, ib, M, CC.s_list, CC.g_list, CC.g_cap,
+                                         CC.ccnt, CC.err);
+                    }
+                }
+                __syncthreads();
+                const unsigned long long cnt = static_cast<unsigned long long>(s_ccnt);
+                barrier(cnt << 32, m, [] {}, [&](unsigned long long x) {
+                    const int tot = static_cast<int>(x >> 32);
+                    bb = m;
+                    set_lim(0, 0);
+                    set_lim(1, m);
+                    if (tot == 0) {
+                        bfs_open = 0;
+                        rho = 1;
+                        tail = m;
+                        fe = m;
+                    } else {
+                        bfs_open = 1;
+                        limk = m;
+                        tail = m + tot;
+                        fe = tail;
+                        set_lim(2, tail);
+                        if (lb == 0) limits[2] = tail;
+                    }
+                    done = !bfs_open && i > rho - 1;
+                    shares_now();
+                    publish();
+                });
+            } else {
+                if (A.given_rho + 1 <= kLimRing) {
+                    for (int r = tid; r <= A.given_rho; r += kBlock) s_lim[r] = ldcg(limits + r);
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    rho = A.given_rho;
+                    use_glim = rho + 1 > kLimRing;
+                    lim_top = rho;
+                    bfs_open = 0;
+                    tail = lim(rho);
+                    bb = lim(1);
+                    fe = rho >= 2 ? lim(2) : tail;
+                    done = i > rho - 1;
+                    shares_now();
+                    publish();
+                }
+                __syncthreads();
+            }
+        } else {
+            // resume a run stopped by max_iters: state from ctl, limits from global
+            if (tid == 0) {
+                k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
+                bfs_open = ctl->bfs_open; done = ctl->done;
+                tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
+                frzb = ctl->s_frzb; frze = ctl->s_frze;
+                use_glim = true;
+                shares_now();
+                publish();
+            }
+            __syncthreads();
+        }
+
+        long long calls = 0, degs = 0;
+        int iters = 0;
+        for (;;) {
+            if (S.done || (A.max_iters > 0 && iters >= A.max_iters)) break;
+            const int kk = S.k;
+            const bool dbg = A.dbg != nullptr && tid == 0 && iters < A.dbg_iters;
+            unsigned long long* dslot =
+                dbg ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
+            if (dbg) dslot[0] = gtimer();
+            const int prv = S.parity, cur_b = prv ^ 1;
+            const T* dp = dist[prv];
+            T* dcur = dist[cur_b];
+            const int* lp = LABELS ? lab[prv] : nullptr;
+            int* lc = LABELS ? lab[cur_b] : nullptr;
+            const int bb_ = S.bb, be_ = S.be, fe_ = S.fe, oe_ = S.oe;
+            const bool expand = S.expand != 0;
+            const bool cached = (be_ - bb_) <= (kCacheSlots - 1) * nb;
+            // owned positions: band task t at p0 + t * nb; the frozen topleset's
+            // positions go to the groups from the top of the CTA down
+            const int p0 = S.p0, a0 = S.a0;
+            const int f0 = S.f0, fa0 = S.fa0, nfz = S.nfz;
+            int nonconv = 0;
+            T my_max = T(0);
+            constexpr int kGroups = kBlock / kGroup;
+            for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
+                const bool act = p0 + t * nb < be_;
+                const bool frz = tf < nfz;
+                if (!__any_sync(kFull, act || frz)) break;
+                const int p = p0 + t * nb;
+                bool ca = false, cb = false;
+                int ia = 0, ib = 0;
+                relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
+                                  cached, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
+                                  expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
+                                  cb, ib, (dbg && t == 0) ? dslot : nullptr);
+                if (expand)
+                    claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
+                                     CC.ccnt, CC.err);
+                if (frz && (tid & (kGroup - 1)) == 0) {
+                    // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
+                    const int fp = f0 + tf * nb;
+                    const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
+                    const int v = tg.x == fp ? tg.y : ldcg(pv + fp);
+                    dcur[v] = ldcg(dp + v);
+                    if (LABELS) lc[v] = ldcg(lp + v);
+                }
+            }
+            if (dbg) dslot[7] = cyc();
+            nonconv = __syncthreads_or(nonconv);
+            if (A.trace != nullptr) {
+                const T bmax = block_max(my_max, red_t);
+                if (tid == 0 && bmax > T(0)) atomicMax(&ctl->slot[kk % 3], Lim<T>::bits(bmax));
+            }
+            if (dbg) dslot[1] = gtimer();
+            const unsigned long long pay =
+                (nonconv ? (1ull << 16) : 0ull) | (static_cast<unsigned long long>(s_ccnt) << 32);
+            int c_p0 = 0, c_a0 = 0, n_p0 = 0, n_a0 = 0, c_nfz = 0;
+            barrier(pay, be_, [&] {
+                first_owned(fe, c_p0, c_a0);  // converged: the band starts at fe
+                first_owned(bb, n_p0, n_a0);  // not converged: it stays at bb
+                c_nfz = owned_count(n_p0, fe);  // converged: [bb, fe) is frozen next
+            }, [&](unsigned long long x) {
+                if (dbg) dslot[2] = gtimer();
+                const int nnc = static_cast<int>((x >> 16) & 0xffffull);
+                const int tot = static_cast<int>(x >> 32);
+                const bool conv = nnc == 0;  // ptp.cpp:114
+                const int ub = bb, ue = S.be;
+                upd += static_cast<unsigned long long>(ue - ub);
+                if (lb == 0 && A.trace != nullptr) {
+                    const int row = kk - A.trace_k0;
+                    if (row >= 0 && row < A.trace_cap) {
+                        TraceRow r;
+                        r.k = kk; r.i = i; r.j = S.j; r.conv = conv ? 1 : 0;
+                        r.updated = ue - ub;
+                        r.max_rel = static_cast<double>(
+                            Lim<T>::from_bits(__ldcg(&ctl->slot[kk % 3])));
+                        A.trace[row] = r;
+                    }
+                }
+                int nt = tail;
+                if (bfs_open) {
+                    if (tot == 0) {
+                        bfs_open = 0;
+                        rho = kk + 1;
+                    } else {
+                        nt = tail + tot;
+                        set_lim(kk + 2, nt);
+                        if (lb == 0) limits[kk + 2] = nt;
+                        limk = tail;
+                    }
+                }
+                if (conv) {
+                    frzb = bb;
+                    frze = fe;
+                    bb = fe;
+                    fe = (i + 2 <= kk + 1) ? pf : nt;
+                    ++i;
+                    sh_p0 = c_p0; sh_a0 = c_a0; sh_f0 = n_p0; sh_fa0 = n_a0; sh_nfz = c_nfz;
+                } else {
+                    frzb = frze = 0;
+                    sh_p0 = n_p0; sh_a0 = n_a0; sh_nfz = 0;
+                }
+                tail = nt;
+                parity ^= 1;
+                k = kk;
+                done = !bfs_open && i > rho - 1;
+                publish();
+                if (dbg) dslot[8] = gtimer();
+            });
+            ++iters;
+        }
+
+        // per-query statistics
+        const long long bc = block_sum(calls, red_l);
+        const long long bd = block_sum(degs, red_l);
+        if (tid == 0) {
+            if (bc) atomicAdd(&ctl->relax, static_cast<unsigned long long>(bc));
+            if (bd) atomicAdd(&ctl->degen, static_cast<unsigned long long>(bd));
+            if (s_err) atomicMax(&ctl->err, s_err);
+            if (lb == 0) {
+                ctl->k = k; ctl->i = i; ctl->rho = rho; ctl->parity = parity;
+                ctl->bfs_open = bfs_open; ctl->done = done;
+                ctl->s_tail = tail; ctl->s_limk = limk; ctl->s_bb = bb; ctl->s_fe = fe;
+                ctl->s_frzb = frzb; ctl->s_frze = frze;
+                ctl->updates += upd;
+            }
+            S.done = done;
+            S.parity = parity;
+        }
+        __syncthreads();
+        const int fin_done = S.done;
+        const int fin = S.parity;  // buffer written last (ptp.cpp:142)
+        if (!fin_done) continue;   // resumable launch ended mid-run
+
+        // copy-out to original vertex order, widened (ptp.cpp:139-147)
+        double vmax = -1.0;
+        int vidx = INT_MAX;
+        if (A.out_dist != nullptr || A.fps_mode || A.out_labels != nullptr) {
+            const T* df = dist[fin];
+            const int* lf = LABELS ? lab[fin] : nullptr;
+            const long long qo = static_cast<long long>(q) * n;
+            for (int v = gtid; v < n; v += gthreads) {
+                const T x = ldcg(df + v);
+                if (A.out_dist != nullptr) {
+                    if (A.out_double)
+                        static_cast<double*>(A.out_dist)[qo + v] = static_cast<double>(x);
+                    else
+                        static_cast<float*>(A.out_dist)[qo + v] = static_cast<float>(x);
+                }
+                if (A.out_labels != nullptr)
+                    A.out_labels[qo + v] = LABELS ? ldcg(lf + v) : (x != inf ? 0 : -1);
+                const double xd = static_cast<double>(x);
+                if (xd > vmax || (xd == vmax && v < vidx)) {
+                    vmax = xd;
+                    vidx = v;
+                }
+            }
+        }
+        if (A.fps_mode) {
+            // block argmax: max value, lowest index (sampling.cpp:29-36)
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(kFull, vmax, o);
+                const int oi = __shfl_xor_sync(kFull, vidx, o);
+                if (ov > vmax || (ov == vmax && oi < vidx)) { vmax = ov; vidx = oi; }
+            }
+            if ((tid & 31) == 0) { red_v[tid >> 5] = vmax; red_i[tid >> 5] = vidx; }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < kBlock / 32; ++w)
+                    if (red_v[w] > vmax || (red_v[w] == vmax && red_i[w] < vidx)) {
+                        vmax = red_v[w];
+                        vidx = red_i[w];
+                    }
+                A.fps_scratch[2 * blockIdx.x] =
+                    static_cast<unsigned long long>(__double_as_longlong(vmax));
+                A.fps_scratch[2 * blockIdx.x + 1] = static_cast<unsigned long long>(vidx);
+            }
+        }
+        barrier(0ull, 0, [] {}, [&](unsigned long long) {
+            if (lb != 0) return;
+            QueryStats st;
+            st.relax = static_cast<long long>(__ldcg(&ctl->relax));
+            st.degen = static_cast<long long>(__ldcg(&ctl->degen));
+            st.updates = static_cast<long long>(ctl->updates);
+            st.iterations = k;
+            st.rho = rho;
+            st.unreached = n - tail;
+            st.done = 1;
+            st.radius = 0.0;
+            st.argmax = -1;
+            const int e = __ldcg(&ctl->err);
+            st.pad = e >= 2 ? e : 0;  // 2: claim list overflow, 3: position never written
+            if (A.fps_mode) {
+                double bv = -1.0;
+                int bi = INT_MAX;
+                for (int b = g * nb; b < g * nb + nb; ++b) {
+                    const double ov = __longlong_as_double(
+                        static_cast<long long>(__ldcg(&A.fps_scratch[2 * b])));
+                    const int oi = static_cast<int>(__ldcg(&A.fps_scratch[2 * b + 1]));
+                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                st.radius = bv;
+                st.argmax = bi;
+                if (!A.fps_final) {
+                    if (ldcg(level + bi) == 0) ctl->err = 1;  // would repeat a sample
+                    A.fps_samples[A.src_count] = bi;
+                }
+            }
+            A.qstats[q] = st;
+        });
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+size_t run4_dyn_smem(int precision, bool) {
+    return kCacheSlots *
+           (precision == 0 ? Cache<float>::bytes_per_slot() : Cache<double>::bytes_per_slot());
+}
+
+const void* run4_kernel_ptr(int precision, bool labels) {
+    if (precision == 0)
+        return labels ? reinterpret_cast<const void*>(&ptp_run4_kernel<float, true>)
+                      : reinterpret_cast<const void*>(&ptp_run4_kernel<float, false>);
+    return labels ? reinterpret_cast<const void*>(&ptp_run4_kernel<double, true>)
+                  : reinterpret_cast<const void*>(&ptp_run4_kernel<double, false>);
+}
+
+}  // namespace gdb

@@ -37,3 +37,9 @@ if okb.any():
     d = np.diff(bp, axis=2)[okb] / 1.965
     print("barrier3 ns (release fence, poll wait, slot reduce): mean", d.mean(0).round(0),
           "p90", np.percentile(d, 90, axis=0).round(0))
+# v4: end of publish (slot 8, globaltimer) relative to release (slot 2)
+pb = t[:, :, 8]
+okp = (pb > 0) & (pb >= t[:, :, 2]) & (pb - t[:, :, 2] < 100000)
+if okp.any() and not okb.any():
+    print("v4 post+publish ns: mean %.0f p90 %.0f" % ((pb - t[:, :, 2])[okp].mean(),
+          np.percentile((pb - t[:, :, 2])[okp], 90)))

@@ -15,11 +15,11 @@ import paper_1810_08218_b200 as g
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["v3", "v2", "v2-wide"], autouse=True)
+@pytest.fixture(params=["v4", "v3", "v2", "v2-wide"], autouse=True)
 def solver(request, monkeypatch):
-    """Run every parity test on all solver paths: the queue-based kernel (v2, default),
-    the same kernel forced onto its thread-per-vertex wide-band path (v2-wide), and the
-    claimer-first kernel with BFS-ordered packed records (v3)."""
+    """Run every parity test on all solver paths: the queue-based kernel (v2), the same
+    kernel forced onto its thread-per-vertex wide-band path (v2-wide), the claimer-first
+    kernel with BFS-ordered packed records (v3) and the owner-cached kernel (v4)."""
     monkeypatch.setenv("GEODIST_SOLVER", request.param[1])
     if request.param == "v2-wide":
         monkeypatch.setenv("GEODIST_WIDE", "0")
