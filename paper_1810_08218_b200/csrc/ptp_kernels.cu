@@ -63,7 +63,7 @@ __global__ void pack_kernel(const double* __restrict__ xyz, int n, const int* __
             const T g12 = dot3(x0, y0, z0, x, y, z);
             T q11, q12, q22, a;
             const bool degen = corner_geometry(g0, g, g12, q11, q12, q22, a);
-            Quad<T>::store(quad, c0 + c, q11, q12, q22, a);
+            Quad<T>::store(quad, c0 + c, q11, q12, q22, quad_w<T>(a, degen));
             if (degen) ring_out[r0 + c] = ring_in[r0 + c] | INT_MIN;
         }
         x0 = x; y0 = y; z0 = z; g0 = g;
@@ -313,8 +313,8 @@ __device__ __forceinline__ void relax_thread(const MeshDev& M, bool act, int p, 
                 q.load(M.equad, static_cast<int>(qb + ell_slot(c)));
                 const bool mixed = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
                 int side, deg;
-                const T val = corner_candidate(t[c], t[c + 1], L[c], L[c + 1], q.q11, q.q12,
-                                               q.q22, q.a, raw[c] < 0, mixed, side, deg);
+                const T val = corner_eval<T>(t[c], t[c + 1], L[c], L[c + 1], q, raw[c] < 0, mixed,
+                                             side, deg);
                 degs += deg;
                 if (val < best) {
                     best = val;
@@ -349,7 +349,7 @@ __device__ __forceinline__ void relax_thread(const MeshDev& M, bool act, int p, 
             q.load(M.quad, c0 + c);
             const bool mixed = LABELS && l0 != l1 && t0 != inf && t1 != inf;
             int side, deg;
-            const T val = corner_candidate(t0, t1, L0, L1, q.q11, q.q12, q.q22, q.a, x0 < 0, mixed,
+            const T val = corner_eval<T>(t0, t1, L0, L1, q, x0 < 0, mixed,
                                            side, deg);
             degs += deg;
             if (val < best) {
@@ -1418,9 +1418,14 @@ __global__ void planar_test_kernel(const double* x1, const double* x2, const dou
     const T g12 = dot3(ax, ay, az, bx, by, bz);
     T q11, q12, q22, a;
     const bool dg = corner_geometry(g11, g22, g12, q11, q12, q22, a);
+    // the solver's own path: the packed quad (4th word per quad_w) and corner_eval
+    Quad<T> qd;
+    qd.q11 = q11;
+    qd.q12 = q12;
+    qd.q22 = q22;
+    qd.a = quad_w<T>(a, dg);
     int s, d;
-    const T v = corner_candidate(to_t<T>(t1[q]), to_t<T>(t2[q]), sq(g11), sq(g22), q11, q12, q22,
-                                 a, dg, false, s, d);
+    const T v = corner_eval<T>(to_t<T>(t1[q]), to_t<T>(t2[q]), sq(g11), sq(g22), qd, dg, false, s, d);
     value[q] = static_cast<double>(v);
     side[q] = s;
     degen[q] = d;

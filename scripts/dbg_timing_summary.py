@@ -1,7 +1,7 @@
 import numpy as np, sys
 raw = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/dbg_timing.bin", "rb").read()
 it, nb = np.frombuffer(raw[:8], np.int32)
-t = np.frombuffer(raw[8:], np.uint64).reshape(it, nb, 12).astype(np.int64)
+t = np.frombuffer(raw[8:], np.uint64).reshape(it, nb, -1).astype(np.int64)
 valid = (t[:, :, 0] > 0).all(axis=1)
 t = t[valid]
 base = t[:, :, 0].min(axis=1, keepdims=True)
@@ -43,3 +43,23 @@ okp = (pb > 0) & (pb >= t[:, :, 2]) & (pb - t[:, :, 2] < 100000)
 if okp.any() and not okb.any():
     print("v4 post+publish ns: mean %.0f p90 %.0f" % ((pb - t[:, :, 2])[okp].mean(),
           np.percentile((pb - t[:, :, 2])[okp], 90)))
+# v4: slowest warp of each CTA (slot 9) vs warp 0 (slot 10): cycles << 8 | flags
+sw = t[:, :, 9]
+w0 = t[:, :, 10]
+if (sw > 0).any():
+    cyc_s = (sw >> 8) / 1.965
+    fl = sw & 0xff
+    print("slowest warp loop ns: mean %.0f p90 %.0f; warp0 mean %.0f" % (cyc_s[sw > 0].mean(),
+          np.percentile(cyc_s[sw > 0], 90), ((w0 >> 8) / 1.965)[w0 > 0].mean()))
+    for name, bit in (("new-topleset task", 1), ("freeze", 2)):
+        print("  slowest warp had %s: %.0f%%" % (name, 100 * ((fl[sw > 0] & bit) > 0).mean()))
+    print("  slowest warp passes: ", np.bincount((fl[sw > 0] >> 3))[:6])
+if (sw > 0).any():
+    print("  slowest warp had fresh task: %.0f%%" % (100 * ((fl[sw > 0] & 4) > 0).mean()))
+if t.shape[2] >= 16:
+    k2 = t[:, :, 11:15].astype(np.float64)
+    ok2 = t[:, :, 13] > 0
+    if ok2.any():
+        print("kind-2 first task (ns from entry): pv %.0f (spins mean %.2f, max %d) row %.0f cas %.0f" % (
+            k2[..., 0][ok2].mean() / 1.965, k2[..., 1][ok2].mean(), k2[..., 1][ok2].max(),
+            k2[..., 2][ok2].mean() / 1.965, k2[..., 3][ok2].mean() / 1.965))
