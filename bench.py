@@ -126,6 +126,8 @@ def config_block(n, precision, nranks):
             "n_vertices": n, "noise_sigma": SIGMA, "noise_rng": "std::mt19937(1) normal",
             "sources_per_field": 1, "precision": precision, "epsilon": 1e-3,
             "l2": "flushed (256 MiB write) between timed steps",
+            "solver": {"2": "v2 ptp_run_kernel", "3": "v3 ptp_run3_kernel"}.get(
+                os.environ.get("GEODIST_SOLVER", "4")[:1], "v4 ptp_run4_kernel"),
             "parallelism": f"independent fields, {nranks} rank(s)"}
 
 

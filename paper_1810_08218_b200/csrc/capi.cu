@@ -319,13 +319,14 @@ void check_config(const geodist_ptp_config* c) {
         throw std::invalid_argument("precision must be 'single' or 'double'");
 }
 
-// Solver kernel: 2 = queue-based kernel (default), 3 = claimer-first kernel with
-// BFS-ordered packed records (GEODIST_SOLVER=3; falls back to 2 on claim-list
-// overflow).  Tests run both.
+// Solver kernel: 4 = owner-cached kernel (default, ptp_run4.cu), 2 = queue-based
+// kernel, 3 = claimer-first kernel with BFS-ordered packed records
+// (GEODIST_SOLVER=2|3; 3 and 4 fall back to 2 on claim-list overflow).  Tests
+// run all of them.
 int solver_version() {
     const char* e = getenv("GEODIST_SOLVER");
-    if (e && (e[0] == '3' || e[0] == '4')) return e[0] - '0';
-    return 2;
+    if (e && (e[0] == '2' || e[0] == '3')) return e[0] - '0';
+    return 4;
 }
 
 // Everything one distance-field solve needs from the caller.

@@ -36,6 +36,7 @@ struct Bcast4 {
     // this CTA's share (positions p == lb mod nb): band tasks p0 + t * nb below
     // be (record-cache slot a0 + t), frozen positions f0 + t * nb for t < nfz
     int p0, a0, f0, fa0, nfz;
+    int nold;  // wide iterations: owned positions in [bb, oe) (pipelined)
 };
 
 constexpr int kCacheSlots = 512;  // record-cache ring (power of two) per CTA
@@ -70,7 +71,7 @@ template <typename T> struct Cache {
     int2* pv;    // (position tag, vertex id)
     T* L;        // |x| of the two entries
     Quad<T>* q;  // Gram quads of corners gl and gl+4
-    static constexpr size_t bytes_per_slot() {
+    __host__ __device__ static constexpr size_t bytes_per_slot() {
         return 4 * (sizeof(int2) + sizeof(int2) + 2 * sizeof(T) + 2 * sizeof(Quad<T>));
     }
     __device__ void bind(unsigned char* base, int R) {
@@ -141,9 +142,20 @@ struct ClaimCtx {
     int* err;
 };
 
+// A task whose record and distances were staged in shared memory by the
+// wide-band pipeline (pipeline_wide).
+template <typename T> struct StageIn {
+    int2 rr;
+    T La, Lb;
+    Quad<T> qa, qb;
+    int v;
+    T ta, tb, tv;
+    int la, lb, lv;
+};
+
 // Relax the vertex at BFS position p (4-lane group; relax_vertex,
 // update_kernel.hpp:93-120).  Lanes return their claims in (ca, ia, cb, ib).
-template <typename T, bool LABELS>
+template <typename T, bool LABELS, bool STAGED = false>
 __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
                                        int sl, bool act, bool is_new, bool cached, int p,
                                        int kk, const int* pv, const int* pring, const T* pL,
@@ -152,7 +164,8 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                                        const ClaimCtx& CC, int& nonconv, T& my_max,
                                        long long& calls, long long& degs, bool& ca_claim,
                                        int& ida, bool& cb_claim, int& idb,
-                                       unsigned long long* tdbg) {
+                                       unsigned long long* tdbg,
+                                       const StageIn<T>& sin = StageIn<T>{}) {
     const T inf = Lim<T>::inf();
     if (tdbg) tdbg[3] = cyc();
     const int gl = threadIdx.x & (kGroup - 1);
@@ -165,7 +178,15 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     qb = qa;
     const int ci = sl * 4 + gl;
     bool hit = false;
-    if (act && cached && !is_new) {
+    if (STAGED) {
+        hit = true;
+        v = sin.v;
+        rr = sin.rr;
+        La = sin.La;
+        Lb = sin.Lb;
+        qa = sin.qa;
+        qb = sin.qb;
+    } else if (act && cached && !is_new) {
         const int2 tg = C.pv[ci];
         if (tg.x == p) {
             hit = true;
@@ -237,19 +258,34 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     }
     T tv = inf;
     int lv = -1;
-    if (act && gl == 0) {
-        tv = ldcg(dp + v);
-        if (LABELS) lv = ldcg(lp + v);
-    }
     T ta = inf, tb = inf;
     int la = -1, lb_ = -1;
-    if (hasa) {
-        ta = ldcg(dp + ida);
-        if (LABELS) la = ldcg(lp + ida);
-    }
-    if (hasb) {
-        tb = ldcg(dp + idb);
-        if (LABELS) lb_ = ldcg(lp + idb);
+    if (STAGED) {
+        if (act && gl == 0) {
+            tv = sin.tv;
+            lv = sin.lv;
+        }
+        if (hasa) {
+            ta = sin.ta;
+            la = sin.la;
+        }
+        if (hasb) {
+            tb = sin.tb;
+            lb_ = sin.lb;
+        }
+    } else {
+        if (act && gl == 0) {
+            tv = ldcg(dp + v);
+            if (LABELS) lv = ldcg(lp + v);
+        }
+        if (hasa) {
+            ta = ldcg(dp + ida);
+            if (LABELS) la = ldcg(lp + ida);
+        }
+        if (hasb) {
+            tb = ldcg(dp + idb);
+            if (LABELS) lb_ = ldcg(lp + idb);
+        }
     }
     if (tdbg) tdbg[5] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv)));
     T best = gl == 0 ? tv : inf;
@@ -334,6 +370,142 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
             if (p < fe && rc > my_max) my_max = rc;
             if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
         }
+    }
+}
+
+// Wide iterations: one band vertex per THREAD from its packed record (no
+// shuffles, no idle corner slots, record bookkeeping once per vertex): the
+// sequential strict-'<' fan scan of relax_vertex (update_kernel.hpp:93-120),
+// corners evaluated two at a time.
+template <typename T> __device__ __forceinline__ void load_L8_cg(const T* base, size_t pb, T* L);
+template <> __device__ __forceinline__ void load_L8_cg<float>(const float* base, size_t pb, float* L) {
+    const float4* q = reinterpret_cast<const float4*>(base + pb);
+    const float4 a = __ldcg(q), b = __ldcg(q + 1);
+    L[0] = a.x; L[4] = a.y; L[1] = a.z; L[5] = a.w;
+    L[2] = b.x; L[6] = b.y; L[3] = b.z; L[7] = b.w;
+}
+template <> __device__ __forceinline__ void load_L8_cg<double>(const double* base, size_t pb, double* L) {
+    const double2* q = reinterpret_cast<const double2*>(base + pb);
+    const double2 a = __ldcg(q), b = __ldcg(q + 1), c = __ldcg(q + 2), d = __ldcg(q + 3);
+    L[0] = a.x; L[4] = a.y; L[1] = b.x; L[5] = b.y;
+    L[2] = c.x; L[6] = c.y; L[3] = d.x; L[7] = d.y;
+}
+
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, int p, int kk,
+                                           const int* pv, const int* pring, const T* pL,
+                                           const char* pquad, const T* dp, T* dc, const int* lp,
+                                           int* lc, int fe, T eps, int& nonconv, T& my_max,
+                                           long long& calls, long long& degs) {
+    const T inf = Lim<T>::inf();
+    const size_t pb = static_cast<size_t>(p) * kEllW;
+    const int v = ldcg(pv + p);
+    int raw[kEllW];
+    T L[kEllW];
+    {
+        const int4* r = reinterpret_cast<const int4*>(pring + pb);
+        const int4 a = __ldcg(r), b = __ldcg(r + 1);
+        raw[0] = a.x; raw[4] = a.y; raw[1] = a.z; raw[5] = a.w;
+        raw[2] = b.x; raw[6] = b.y; raw[3] = b.z; raw[7] = b.w;
+    }
+    load_L8_cg<T>(pL, pb, L);
+    const T tv = ldcg(dp + v);
+    const int lv = LABELS ? ldcg(lp + v) : -1;
+    int d = (raw[0] >> kMetaShift) & 15;
+    T best = tv;
+    int blab = lv;
+    if (d == kEllOverflow) {
+        // more than 7 corners: CSR tables, sequential fan walk
+        const int c0 = __ldg(M.cptr + v);
+        d = __ldg(M.cptr + v + 1) - c0;
+        const int r0 = c0 + v;
+        const T* ringL = static_cast<const T*>(M.ringL);
+        int x0 = __ldg(M.ring + r0);
+        int i0 = x0 & INT_MAX;
+        T t0 = ldcg(dp + i0), L0 = __ldg(ringL + r0);
+        int l0 = LABELS ? ldcg(lp + i0) : -1;
+        for (int c = 0; c < d; ++c) {
+            const int x1 = __ldg(M.ring + r0 + c + 1);
+            const int i1 = x1 & INT_MAX;
+            const T t1 = ldcg(dp + i1), L1 = __ldg(ringL + r0 + c + 1);
+            const int l1 = LABELS ? ldcg(lp + i1) : -1;
+            Quad<T> q;
+            q.load(M.quad, c0 + c);
+            const bool mixed = LABELS && l0 != l1 && t0 != inf && t1 != inf;
+            int side, deg;
+            const T val = corner_eval<T>(t0, t1, L0, L1, q, x0 < 0, mixed, side, deg);
+            degs += deg;
+            if (val < best) {
+                best = val;
+                if (LABELS) blab = side == 0 ? l0 : l1;
+            }
+            x0 = x1; i0 = i1; t0 = t1; L0 = L1; l0 = l1;
+        }
+    } else if (d > 0) {
+        T t[kEllW + 1];
+        int l[kEllW + 1];
+#pragma unroll
+        for (int e = 0; e <= kEllW; ++e) {
+            t[e] = inf;
+            l[e] = -1;
+            if (e < kEllW && e <= d) {
+                t[e] = ldcg(dp + (raw[e] & kIdMask));
+                if (LABELS) l[e] = ldcg(lp + (raw[e] & kIdMask));
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kEllW - 1; c += 2) {
+            Quad<T> q0, q1;
+            q0.load_cg(pquad, pb + ell_slot(c));
+            q1.load_cg(pquad, pb + ell_slot(c + 1));
+            const bool m0 = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
+            const bool m1 = LABELS && l[c + 1] != l[c + 2] && t[c + 1] != inf && t[c + 2] != inf;
+            T val[2];
+            int side[2], deg[2];
+            if constexpr (sizeof(T) == 4) {
+                const float t1v[2] = {t[c], t[c + 1]}, t2v[2] = {t[c + 1], t[c + 2]};
+                const float L1v[2] = {L[c], L[c + 1]};
+                const float L2v[2] = {L[c + 1], c + 2 < kEllW ? L[c + 2] : 0.0f};
+                const Quad<float> qv[2] = {q0, q1};
+                const bool dgv[2] = {raw[c] < 0, raw[c + 1] < 0};
+                const bool mix[2] = {m0, m1};
+                const bool valid[2] = {c < d, c + 1 < d};
+                corner_pair_f32(t1v, t2v, L1v, L2v, qv, dgv, mix, valid, val, side, deg);
+            } else {
+                val[0] = corner_eval<T>(t[c], t[c + 1], L[c], L[c + 1], q0, raw[c] < 0, m0,
+                                        side[0], deg[0]);
+                if (c + 1 < d)
+                    val[1] = corner_eval<T>(t[c + 1], t[c + 2], L[c + 1], L[c + 2 < kEllW ? c + 2 : c + 1],
+                                            q1, raw[c + 1] < 0, m1, side[1], deg[1]);
+                else {
+                    val[1] = inf;
+                    deg[1] = 0;
+                    side[1] = -1;
+                }
+                if (!(c < d)) {
+                    val[0] = inf;
+                    deg[0] = 0;
+                }
+            }
+            degs += deg[0] + deg[1];
+            if (c < d && val[0] < best) {
+                best = val[0];
+                if (LABELS) blab = side[0] == 0 ? l[c] : l[c + 1];
+            }
+            if (c + 1 < d && val[1] < best) {
+                best = val[1];
+                if (LABELS) blab = side[1] == 0 ? l[c + 1] : l[c + 2];
+            }
+        }
+    }
+    dc[v] = best;
+    if (LABELS) lc[v] = blab;
+    calls += d;
+    if (p < fe || A.last_change != nullptr) {
+        const T rc = rel_change(tv, best);
+        if (p < fe && rc >= eps) nonconv = 1;
+        if (p < fe && rc > my_max) my_max = rc;
+        if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
     }
 }
 
@@ -489,6 +661,11 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if (A.trace != nullptr && lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
             S.p0 = sh_p0;
             S.a0 = sh_a0;
+            {
+                const int oe = bfs_open ? limk : be;
+                S.nold = ((A.wide_factor == 0 || be - bb > (kCacheSlots - 1) * nb) && oe > sh_p0)
+                             ? div_nb(oe - sh_p0 + nb - 1) : 0;
+            }
             S.f0 = sh_f0;
             S.fa0 = sh_fa0;
             S.nfz = sh_nfz;
@@ -656,7 +833,8 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             int* lc = LABELS ? lab[cur_b] : nullptr;
             const int bb_ = S.bb, be_ = S.be, fe_ = S.fe, oe_ = S.oe;
             const bool expand = S.expand != 0;
-            const bool cached = (be_ - bb_) <= (kCacheSlots - 1) * nb;
+            // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
+            const bool cached = A.wide_factor != 0 && (be_ - bb_) <= (kCacheSlots - 1) * nb;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
             const int p0 = S.p0, a0 = S.a0;
@@ -664,7 +842,10 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             int nonconv = 0;
             T my_max = T(0);
             constexpr int kGroups = kBlock / kGroup;
-            for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
+            // wide iterations (band beyond the record cache): the generic loop takes only
+            // the newest topleset; older positions go through pipeline_wide below
+            const int nold = cached ? 0 : S.nold;
+            for (int t = nold + tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
                 const bool act = p0 + t * nb < be_;
                 const bool frz = tf < nfz;
                 if (!__any_sync(kFull, act || frz)) break;
@@ -686,6 +867,12 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     dcur[v] = ldcg(dp + v);
                     if (LABELS) lc[v] = ldcg(lp + v);
                 }
+            }
+            if (!cached) {
+                // older band positions: one vertex per thread
+                for (int t = tid; t < nold; t += kBlock)
+                    relax_wide<T, LABELS>(M, A, p0 + t * nb, kk, pv, pring, pL, pquad, dp, dcur,
+                                          lp, lc, fe_, eps, nonconv, my_max, calls, degs);
             }
             if (dbg) dslot[7] = cyc();
             nonconv = __syncthreads_or(nonconv);

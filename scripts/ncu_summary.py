@@ -23,6 +23,11 @@ WANT = {
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_throughput_pct",
     "smsp__cycles_active.avg": "smsp_cycles_active",
+    "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors",
+    "lts__t_sectors_srcunit_tex_op_write.sum": "l2_write_sectors",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "launch__func_cache_config": "func_cache_config",
 }
 UNITS = {"dram_read": None, "dram_write": None, "l2_bytes": None}
 
@@ -72,8 +77,13 @@ def summarise(rep):
 def main():
     out = {}
     for rep in sys.argv[1:]:
-        key = "ptp_run_kernel_" + ("double" if "double" in rep else "single")
+        base = os.path.basename(rep).replace(".ncu-rep", "")
+        if "torus" in base:
+            key = "torus_" + ("double" if "double" in base else "single")
+        else:
+            key = "ptp_run_kernel_" + ("double" if "double" in base else "single")
         out[key] = summarise(rep)
+        out[key]["kernel"] = "ptp_run4_kernel (v4)"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     old = {}

@@ -15,13 +15,14 @@ import paper_1810_08218_b200 as g
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["v4", "v3", "v2", "v2-wide"], autouse=True)
+@pytest.fixture(params=["v4", "v4-wide", "v3", "v2", "v2-wide"], autouse=True)
 def solver(request, monkeypatch):
-    """Run every parity test on all solver paths: the queue-based kernel (v2), the same
-    kernel forced onto its thread-per-vertex wide-band path (v2-wide), the claimer-first
-    kernel with BFS-ordered packed records (v3) and the owner-cached kernel (v4)."""
+    """Run every parity test on all solver paths: the owner-cached kernel (v4, default)
+    and its thread-per-vertex wide-band path forced on every iteration (v4-wide), the
+    queue-based kernel (v2) and its wide path (v2-wide), and the claimer-first kernel
+    with BFS-ordered packed records (v3)."""
     monkeypatch.setenv("GEODIST_SOLVER", request.param[1])
-    if request.param == "v2-wide":
+    if request.param.endswith("-wide"):
         monkeypatch.setenv("GEODIST_WIDE", "0")
     else:
         monkeypatch.delenv("GEODIST_WIDE", raising=False)
