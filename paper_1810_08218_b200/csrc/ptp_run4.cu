@@ -842,9 +842,11 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             int nonconv = 0;
             T my_max = T(0);
             constexpr int kGroups = kBlock / kGroup;
-            // wide iterations (band beyond the record cache): the generic loop takes only
-            // the newest topleset; older positions go through pipeline_wide below
-            const int nold = cached ? 0 : S.nold;
+            // wide iterations (band beyond the record cache, fp32): the generic loop takes
+            // only the newest topleset; older positions are relaxed one per thread below
+            // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
+            constexpr bool kThreadWide = sizeof(T) == 4;
+            const int nold = (cached || !kThreadWide) ? 0 : S.nold;
             for (int t = nold + tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
                 const bool act = p0 + t * nb < be_;
                 const bool frz = tf < nfz;
@@ -868,7 +870,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     if (LABELS) lc[v] = ldcg(lp + v);
                 }
             }
-            if (!cached) {
+            if constexpr (kThreadWide) {
                 // older band positions: one vertex per thread
                 for (int t = tid; t < nold; t += kBlock)
                     relax_wide<T, LABELS>(M, A, p0 + t * nb, kk, pv, pring, pL, pquad, dp, dcur,
