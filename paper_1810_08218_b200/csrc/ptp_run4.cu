@@ -30,6 +30,11 @@ namespace gdb {
 namespace {
 
 constexpr int kLimRing = 1024;  // topleset limits kept on chip (levels)
+// pv[p] flag: the packed record at position p has been written.  Packed records
+// are only written once the band approaches the record cache's capacity (they
+// serve the wide path); writing them on every first relaxation would stream
+// n * 192 B through the L2 and evict the distance and level arrays.
+constexpr int kPacked = 1 << 30;
 
 struct Bcast4 {
     int k, i, j, bb, oe, be, fe, frzb, frze, parity, done, expand;
@@ -157,17 +162,21 @@ template <typename T> struct StageIn {
 // update_kernel.hpp:93-120).  Lanes return their claims in (ca, ia, cb, ib).
 template <typename T, bool LABELS, bool STAGED = false>
 __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
-                                       int sl, bool act, bool is_new, bool cached, int p,
-                                       int kk, const int* pv, const int* pring, const T* pL,
+                                       int sl, bool act, bool is_new, bool cached, bool pack,
+                                       int p, int kk, const int* pv, const int* pring, const T* pL,
                                        const char* pquad, const T* dp, T* dc, const int* lp,
                                        int* lc, int fe, bool expand, int* level, T eps,
                                        const ClaimCtx& CC, int& nonconv, T& my_max,
                                        long long& calls, long long& degs, bool& ca_claim,
                                        int& ida, bool& cb_claim, int& idb,
                                        unsigned long long* tdbg,
-                                       const StageIn<T>& sin = StageIn<T>{}) {
+                                       const StageIn<T>& sin = StageIn<T>{},
+                                       unsigned long long* kdbg = nullptr,
+                                       unsigned long long it0 = 0) {
     const T inf = Lim<T>::inf();
     if (tdbg) tdbg[3] = cyc();
+    const unsigned long long k0 = kdbg ? cyc() : 0ull;
+    if (kdbg) kdbg[10] = k0 - it0;
     const int gl = threadIdx.x & (kGroup - 1);
     const int g0 = (threadIdx.x & 31) & ~(kGroup - 1);
     int v = 0;
@@ -211,26 +220,34 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                 }
                 v = ld_relaxed_i32(pv + p);
             }
-        } else {
-            v = ldcg(pv + p);
+            if (kdbg) kdbg[11] = gtimer_after(v) - k0;
         }
-        if (is_new) {
-            // first relaxation: the id-indexed ELL row (pulled into L2 by the
-            // claimer), committed to the packed record at the position
+        bool packed = false;
+        if (!is_new) {
+            // packed record (if it was written) and the id, in one trip
+            const int vr = ldcg(pv + p);
+            rr = __ldcg(reinterpret_cast<const int2*>(pring) + (pb >> 1) + gl);
+            Ell2<T>::load_cg(pL, pb + 2 * gl, La, Lb);
+            qa.load_cg(pquad, pb + 2 * gl);
+            qb.load_cg(pquad, pb + 2 * gl + 1);
+            packed = (vr & kPacked) != 0;
+            v = vr & kIdMask;
+        }
+        if (!packed) {
+            // first relaxation (or no packed record): the id-indexed ELL row (pulled
+            // into L2 by the claimer)
             const size_t eb = static_cast<size_t>(v) * kEllW;
             rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
             Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
             qa.load(M.equad, static_cast<int>(eb + 2 * gl));
             qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
-            reinterpret_cast<int2*>(const_cast<int*>(pring))[(pb >> 1) + gl] = rr;
-            Ell2<T>::store(const_cast<T*>(pL), pb + 2 * gl, La, Lb);
-            qa.store_at(const_cast<char*>(pquad), pb + 2 * gl);
-            qb.store_at(const_cast<char*>(pquad), pb + 2 * gl + 1);
-        } else {
-            rr = __ldcg(reinterpret_cast<const int2*>(pring) + (pb >> 1) + gl);
-            Ell2<T>::load_cg(pL, pb + 2 * gl, La, Lb);
-            qa.load_cg(pquad, pb + 2 * gl);
-            qb.load_cg(pquad, pb + 2 * gl + 1);
+            if (is_new && pack) {
+                reinterpret_cast<int2*>(const_cast<int*>(pring))[(pb >> 1) + gl] = rr;
+                Ell2<T>::store(const_cast<T*>(pL), pb + 2 * gl, La, Lb);
+                qa.store_at(const_cast<char*>(pquad), pb + 2 * gl);
+                qb.store_at(const_cast<char*>(pquad), pb + 2 * gl + 1);
+                if (gl == 0) const_cast<int*>(pv)[p] = v | kPacked;
+            }
         }
         if (cached) {
             C.pv[ci] = make_int2(p, v);
@@ -242,6 +259,7 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
         }
     }
     if (tdbg) tdbg[4] = gtimer_after(rr.x + v);
+    if (kdbg) kdbg[12] = gtimer_after(rr.x + rr.y + __float_as_int(static_cast<float>(La + qa.q11 + qb.q11))) - k0;
     const int meta = __shfl_sync(kFull, rr.x, g0);
     int d = act ? (meta >> kMetaShift) & 15 : 0;
     const bool ovf = d == kEllOverflow;
@@ -288,12 +306,15 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
         }
     }
     if (tdbg) tdbg[5] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv)));
+    if (kdbg) kdbg[13] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv))) - k0;
     T best = gl == 0 ? tv : inf;
     int bidx = gl == 0 ? -1 : INT_MAX;
     int blab = gl == 0 ? lv : -1;
     chunk_candidates<T, LABELS>(gl, 0, ovf ? 0 : d, rr.x, rr.y, La, Lb, ta, tb, la, lb_, qa, qb,
                                 best, bidx, blab, degs);
     if (tdbg) tdbg[6] = gtimer_after(__float_as_int(static_cast<float>(best)));
+    if (kdbg) kdbg[14] = gtimer_after(__float_as_int(static_cast<float>(best))) - k0;
+    if (kdbg) kdbg[15] = gtimer_after(static_cast<int>(ca_claim) + static_cast<int>(cb_claim)) - k0;
 
     // overflow vertices (> 7 corners): CSR tables, 7 corners per chunk; their
     // claims are appended one by one (rare: valence > 7)
@@ -398,17 +419,28 @@ __device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, i
                                            int* lc, int fe, T eps, int& nonconv, T& my_max,
                                            long long& calls, long long& degs) {
     const T inf = Lim<T>::inf();
-    const size_t pb = static_cast<size_t>(p) * kEllW;
-    const int v = ldcg(pv + p);
+    size_t pb = static_cast<size_t>(p) * kEllW;
+    const int vr = ldcg(pv + p);
+    const int v = vr & kIdMask;
+    const int* rsrc = pring;
+    const T* lsrc = pL;
+    const char* qsrc = pquad;
+    if (!(vr & kPacked)) {
+        // no packed record (the vertex entered the band while it was narrow): ELL by id
+        pb = static_cast<size_t>(v) * kEllW;
+        rsrc = M.ering;
+        lsrc = static_cast<const T*>(M.eL);
+        qsrc = static_cast<const char*>(M.equad);
+    }
     int raw[kEllW];
     T L[kEllW];
     {
-        const int4* r = reinterpret_cast<const int4*>(pring + pb);
+        const int4* r = reinterpret_cast<const int4*>(rsrc + pb);
         const int4 a = __ldcg(r), b = __ldcg(r + 1);
         raw[0] = a.x; raw[4] = a.y; raw[1] = a.z; raw[5] = a.w;
         raw[2] = b.x; raw[6] = b.y; raw[3] = b.z; raw[7] = b.w;
     }
-    load_L8_cg<T>(pL, pb, L);
+    load_L8_cg<T>(lsrc, pb, L);
     const T tv = ldcg(dp + v);
     const int lv = LABELS ? ldcg(lp + v) : -1;
     int d = (raw[0] >> kMetaShift) & 15;
@@ -456,8 +488,8 @@ __device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, i
 #pragma unroll
         for (int c = 0; c < kEllW - 1; c += 2) {
             Quad<T> q0, q1;
-            q0.load_cg(pquad, pb + ell_slot(c));
-            q1.load_cg(pquad, pb + ell_slot(c + 1));
+            q0.load_cg(qsrc, pb + ell_slot(c));
+            q1.load_cg(qsrc, pb + ell_slot(c + 1));
             const bool m0 = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
             const bool m1 = LABELS && l[c + 1] != l[c + 2] && t[c + 1] != inf && t[c + 2] != inf;
             T val[2];
@@ -719,13 +751,14 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 for (long long x = gtid; x < static_cast<long long>(reach) * kEllW;
                      x += gthreads) {
                     const int p = static_cast<int>(x / kEllW), slot = static_cast<int>(x % kEllW);
-                    const int v = ldcg(pv + p);
+                    const int v = ldcg(pv + p) & kIdMask;
                     const size_t eb = static_cast<size_t>(v) * kEllW + slot;
                     pring[x] = __ldg(M.ering + eb);
                     pL[x] = __ldg(static_cast<const T*>(M.eL) + eb);
                     Quad<T> qq;
                     qq.load(M.equad, static_cast<int>(eb));
                     qq.store_at(pquad, x);
+                    if (slot == 0) pv[p] = v | kPacked;
                 }
             }
             if (tid == 0) s_ccnt = 0;
@@ -738,7 +771,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     if (!__any_sync(kFull, act)) break;
                     int v = 0, c0 = 0, d = 0;
                     if (act) {
-                        v = ldcg(pv + t);
+                        v = ldcg(pv + t) & kIdMask;
                         c0 = __ldg(M.cptr + v);
                         d = __ldg(M.cptr + v + 1) - c0;
                     }
@@ -826,6 +859,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             unsigned long long* dslot =
                 dbg ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
             if (dbg) dslot[0] = gtimer();
+            const unsigned long long it0 = A.dbg != nullptr ? cyc() : 0ull;
             const int prv = S.parity, cur_b = prv ^ 1;
             const T* dp = dist[prv];
             T* dcur = dist[cur_b];
@@ -835,6 +869,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             const bool expand = S.expand != 0;
             // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
             const bool cached = A.wide_factor != 0 && (be_ - bb_) <= (kCacheSlots - 1) * nb;
+            const bool pack = !cached || 2 * (be_ - bb_) > (kCacheSlots - 1) * nb;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
             const int p0 = S.p0, a0 = S.a0;
@@ -854,18 +889,25 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 const int p = p0 + t * nb;
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
+                unsigned long long* kd =
+                    (A.dbg != nullptr && iters < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
+                     (tid & (kGroup - 1)) == 0)
+                        ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x)
+                        : nullptr;
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
-                                  cached, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
+                                  cached, pack, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
                                   expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
-                                  cb, ib, (dbg && t == 0) ? dslot : nullptr);
+                                  cb, ib, (dbg && t == 0) ? dslot : nullptr, StageIn<T>{},
+                                  kd, it0);
                 if (expand)
                     claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
                                      CC.ccnt, CC.err);
+                if (kd) kd[9] = cyc() - it0;
                 if (frz && (tid & (kGroup - 1)) == 0) {
                     // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
                     const int fp = f0 + tf * nb;
                     const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
-                    const int v = tg.x == fp ? tg.y : ldcg(pv + fp);
+                    const int v = tg.x == fp ? tg.y : (ldcg(pv + fp) & kIdMask);
                     dcur[v] = ldcg(dp + v);
                     if (LABELS) lc[v] = ldcg(lp + v);
                 }

@@ -63,3 +63,11 @@ if t.shape[2] >= 16:
         print("kind-2 first task (ns from entry): pv %.0f (spins mean %.2f, max %d) row %.0f cas %.0f" % (
             k2[..., 0][ok2].mean() / 1.965, k2[..., 1][ok2].mean(), k2[..., 1][ok2].max(),
             k2[..., 2][ok2].mean() / 1.965, k2[..., 3][ok2].mean() / 1.965))
+# v4: stages of the CTA's first newest-topleset task (cycles; slots 9-15)
+if t.shape[2] >= 16:
+    kd = t[:, :, 9:16].astype(np.float64) / 1.965
+    ok = (t[:, :, 9] > 0) & (t[:, :, 12] > 0)
+    if ok.any():
+        m = kd[ok].mean(0)
+        print("first new-topleset task (ns): entry@%.0f  pv +%.0f  row +%.0f  dist +%.0f  candidates +%.0f  cas +%.0f  loop-end@%.0f" % (
+            m[1], m[2], m[3], m[4], m[5], m[6], m[0]))
