@@ -881,8 +881,16 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             // only the newest topleset; older positions are relaxed one per thread below
             // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
             constexpr bool kThreadWide = sizeof(T) == 4;
-            const int nold = (cached || !kThreadWide) ? 0 : S.nold;
-            for (int t = nold + tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
+            // Wide iterations (fp32): positions are dealt to CTAs in chunks of 32
+            // consecutive positions (chunk c -> CTA c mod nb) instead of one by one, so
+            // a warp works on 32 neighbouring positions: their records are adjacent and,
+            // since a CTA's claims come from its own chunks, their neighbours' distances
+            // share sectors.  The newest topleset keeps the 4-lane groups (BFS claims),
+            // the older ones are relaxed one vertex per thread.
+            constexpr int kChunk = 32;
+            const bool wchunk = !cached && kThreadWide;
+            if (!wchunk) {
+            for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
                 const bool act = p0 + t * nb < be_;
                 const bool frz = tf < nfz;
                 if (!__any_sync(kFull, act || frz)) break;
@@ -912,11 +920,47 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     if (LABELS) lc[v] = ldcg(lp + v);
                 }
             }
-            if constexpr (kThreadWide) {
-                // older band positions: one vertex per thread
-                for (int t = tid; t < nold; t += kBlock)
-                    relax_wide<T, LABELS>(M, A, p0 + t * nb, kk, pv, pring, pL, pquad, dp, dcur,
-                                          lp, lc, fe_, eps, nonconv, my_max, calls, degs);
+            } else {
+            for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
+                const int p = oe_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
+                const bool act = p < be_;
+                const bool frz = tf < nfz;
+                if (!__any_sync(kFull, act || frz)) break;
+                bool ca = false, cb = false;
+                int ia = 0, ib = 0;
+                unsigned long long* kd =
+                    (A.dbg != nullptr && iters < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
+                     (tid & (kGroup - 1)) == 0)
+                        ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x)
+                        : nullptr;
+                relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
+                                  cached, pack, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
+                                  expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
+                                  cb, ib, (dbg && t == 0) ? dslot : nullptr, StageIn<T>{},
+                                  kd, it0);
+                if (expand)
+                    claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
+                                     CC.ccnt, CC.err);
+                if (kd) kd[9] = cyc() - it0;
+                if (frz && (tid & (kGroup - 1)) == 0) {
+                    // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
+                    const int fp = f0 + tf * nb;
+                    const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
+                    const int v = tg.x == fp ? tg.y : (ldcg(pv + fp) & kIdMask);
+                    dcur[v] = ldcg(dp + v);
+                    if (LABELS) lc[v] = ldcg(lp + v);
+                }
+            }
+            {
+                // older band positions [bb, oe): one vertex per thread, chunked
+                for (int t = tid;; t += kBlock) {
+                    const int p = bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
+                    if (p - (t % kChunk) >= oe_) break;
+                    if (p < oe_)
+                        relax_wide<T, LABELS>(M, A, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc,
+                                              fe_, eps, nonconv, my_max, calls, degs);
+                }
+            }
             }
             if (dbg) dslot[7] = cyc();
             nonconv = __syncthreads_or(nonconv);
