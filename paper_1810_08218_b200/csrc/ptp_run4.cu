@@ -226,10 +226,14 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
         if (!is_new) {
             // packed record (if it was written) and the id, in one trip
             const int vr = ldcg(pv + p);
-            rr = __ldcg(reinterpret_cast<const int2*>(pring) + (pb >> 1) + gl);
-            Ell2<T>::load_cg(pL, pb + 2 * gl, La, Lb);
-            qa.load_cg(pquad, pb + 2 * gl);
-            qb.load_cg(pquad, pb + 2 * gl + 1);
+            // packed records are slot-major (slot s of position p at s * N + p)
+            const size_t N = static_cast<size_t>(A.stride);
+            const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
+            rr = make_int2(__ldcg(pring + s0), __ldcg(pring + s1));
+            La = ldcg(pL + s0);
+            Lb = ldcg(pL + s1);
+            qa.load_cg(pquad, s0);
+            qb.load_cg(pquad, s1);
             packed = (vr & kPacked) != 0;
             v = vr & kIdMask;
         }
@@ -242,10 +246,14 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
             qa.load(M.equad, static_cast<int>(eb + 2 * gl));
             qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
             if (is_new && pack) {
-                reinterpret_cast<int2*>(const_cast<int*>(pring))[(pb >> 1) + gl] = rr;
-                Ell2<T>::store(const_cast<T*>(pL), pb + 2 * gl, La, Lb);
-                qa.store_at(const_cast<char*>(pquad), pb + 2 * gl);
-                qb.store_at(const_cast<char*>(pquad), pb + 2 * gl + 1);
+                const size_t N = static_cast<size_t>(A.stride);
+                const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
+                const_cast<int*>(pring)[s0] = rr.x;
+                const_cast<int*>(pring)[s1] = rr.y;
+                const_cast<T*>(pL)[s0] = La;
+                const_cast<T*>(pL)[s1] = Lb;
+                qa.store_at(const_cast<char*>(pquad), s0);
+                qb.store_at(const_cast<char*>(pquad), s1);
                 if (gl == 0) const_cast<int*>(pv)[p] = v | kPacked;
             }
         }
@@ -419,28 +427,29 @@ __device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, i
                                            int* lc, int fe, T eps, int& nonconv, T& my_max,
                                            long long& calls, long long& degs) {
     const T inf = Lim<T>::inf();
-    size_t pb = static_cast<size_t>(p) * kEllW;
     const int vr = ldcg(pv + p);
     const int v = vr & kIdMask;
+    // packed records are slot-major (slot s of position p at s * N + p): a warp on 32
+    // consecutive positions reads each slot as one contiguous run
+    size_t pb = static_cast<size_t>(p), step = static_cast<size_t>(A.stride);
     const int* rsrc = pring;
     const T* lsrc = pL;
     const char* qsrc = pquad;
     if (!(vr & kPacked)) {
         // no packed record (the vertex entered the band while it was narrow): ELL by id
         pb = static_cast<size_t>(v) * kEllW;
+        step = 1;
         rsrc = M.ering;
         lsrc = static_cast<const T*>(M.eL);
         qsrc = static_cast<const char*>(M.equad);
     }
     int raw[kEllW];
     T L[kEllW];
-    {
-        const int4* r = reinterpret_cast<const int4*>(rsrc + pb);
-        const int4 a = __ldcg(r), b = __ldcg(r + 1);
-        raw[0] = a.x; raw[4] = a.y; raw[1] = a.z; raw[5] = a.w;
-        raw[2] = b.x; raw[6] = b.y; raw[3] = b.z; raw[7] = b.w;
+#pragma unroll
+    for (int e = 0; e < kEllW; ++e) {
+        raw[e] = __ldcg(rsrc + pb + ell_slot(e) * step);
+        L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
     }
-    load_L8_cg<T>(lsrc, pb, L);
     const T tv = ldcg(dp + v);
     const int lv = LABELS ? ldcg(lp + v) : -1;
     int d = (raw[0] >> kMetaShift) & 15;
@@ -488,8 +497,8 @@ __device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, i
 #pragma unroll
         for (int c = 0; c < kEllW - 1; c += 2) {
             Quad<T> q0, q1;
-            q0.load_cg(qsrc, pb + ell_slot(c));
-            q1.load_cg(qsrc, pb + ell_slot(c + 1));
+            q0.load_cg(qsrc, pb + ell_slot(c) * step);
+            q1.load_cg(qsrc, pb + ell_slot(c + 1) * step);
             const bool m0 = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
             const bool m1 = LABELS && l[c + 1] != l[c + 2] && t[c + 1] != inf && t[c + 2] != inf;
             T val[2];
@@ -753,11 +762,12 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     const int p = static_cast<int>(x / kEllW), slot = static_cast<int>(x % kEllW);
                     const int v = ldcg(pv + p) & kIdMask;
                     const size_t eb = static_cast<size_t>(v) * kEllW + slot;
-                    pring[x] = __ldg(M.ering + eb);
-                    pL[x] = __ldg(static_cast<const T*>(M.eL) + eb);
+                    const size_t dst = static_cast<size_t>(slot) * A.stride + p;  // slot-major
+                    pring[dst] = __ldg(M.ering + eb);
+                    pL[dst] = __ldg(static_cast<const T*>(M.eL) + eb);
                     Quad<T> qq;
                     qq.load(M.equad, static_cast<int>(eb));
-                    qq.store_at(pquad, x);
+                    qq.store_at(pquad, dst);
                     if (slot == 0) pv[p] = v | kPacked;
                 }
             }
@@ -888,7 +898,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             // share sectors.  The newest topleset keeps the 4-lane groups (BFS claims),
             // the older ones are relaxed one vertex per thread.
             constexpr int kChunk = 32;
-            const bool wchunk = !cached && kThreadWide;
+            const bool wchunk = !cached;
             if (!wchunk) {
             for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
                 const bool act = p0 + t * nb < be_;
@@ -922,7 +932,9 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             }
             } else {
             for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
-                const int p = oe_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
+                // fp32: the newest topleset here, older ones in relax_wide below; fp64: all
+                const int wbase = kThreadWide ? oe_ : bb_;
+                const int p = wbase + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
                 const bool act = p < be_;
                 const bool frz = tf < nfz;
                 if (!__any_sync(kFull, act || frz)) break;
@@ -951,7 +963,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     if (LABELS) lc[v] = ldcg(lp + v);
                 }
             }
-            {
+            if (kThreadWide) {
                 // older band positions [bb, oe): one vertex per thread, chunked
                 for (int t = tid;; t += kBlock) {
                     const int p = bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
