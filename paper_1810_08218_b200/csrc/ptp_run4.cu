@@ -41,7 +41,6 @@ struct Bcast4 {
     // this CTA's share (positions p == lb mod nb): band tasks p0 + t * nb below
     // be (record-cache slot a0 + t), frozen positions f0 + t * nb for t < nfz
     int p0, a0, f0, fa0, nfz;
-    int nold;  // wide iterations: owned positions in [bb, oe) (pipelined)
 };
 
 constexpr int kCacheSlots = 512;  // record-cache ring (power of two) per CTA
@@ -54,10 +53,10 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ unsigned long long atom_release_add_u64(unsigned long long* p,
+__device__ __forceinline__ unsigned long long atom_acq_rel_add_u64(unsigned long long* p,
                                                                    unsigned long long x) {
     unsigned long long r;
-    asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(x) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(x) : "memory");
     return r;
 }
 __device__ __forceinline__ int ld_relaxed_i32(const int* p) {
@@ -605,8 +604,11 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
     // arrived earlier, i.e. this CTA's offset inside the new topleset, and warp
     // 0 writes the CTA's claim list to those positions.  Readers of the new
     // positions (the owners, next iteration) wait for pv[p] >= 0.
-    auto barrier = [&](unsigned long long payload, int level_start, auto&& pre, auto&& post) {
-        __syncthreads();
+    // The last CTA to arrive learns from its own atomic that the barrier is complete
+    // (acq_rel: it also acquires every earlier arrival) and skips the polling trip.
+    auto barrier = [&](unsigned long long payload, int level_start, auto&& pre, auto&& post,
+                       bool presynced = false) {
+        if (!presynced) __syncthreads();
         if (tid < 32) {
             unsigned long long* w = barw + (bseq & 3);
             unsigned long long old = 0;
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 // word (bseq+2)&3 was last polled at barrier bseq-2; every CTA has
                 // arrived at bseq-1 since, so it is free until barrier bseq+2
                 if (lb == 0) st_relaxed_u64(barw + ((bseq + 2) & 3), 0ull);
-                old = atom_release_add_u64(w, payload + 1ull);
+                old = atom_acq_rel_add_u64(w, payload + 1ull);
                 pre();  // overlaps the arrival's round trip
             }
             const int cnt = static_cast<int>(payload >> 32);
@@ -624,10 +626,12 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     pv[at + x] = x < kSmemClaims ? s_list[x] : g_list[x - kSmemClaims];
             }
             if (tid == 0) {
-                unsigned long long x;
-                do {
-                    x = ld_acquire_u64(w);
-                } while (static_cast<int>(x & 0xffffull) < nb);
+                unsigned long long x = old + payload + 1ull;
+                if (static_cast<int>(x & 0xffffull) < nb) {
+                    do {
+                        x = ld_acquire_u64(w);
+                    } while (static_cast<int>(x & 0xffffull) < nb);
+                }
                 post(x);
             }
         }
@@ -702,11 +706,6 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if (A.trace != nullptr && lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
             S.p0 = sh_p0;
             S.a0 = sh_a0;
-            {
-                const int oe = bfs_open ? limk : be;
-                S.nold = ((A.wide_factor == 0 || be - bb > (kCacheSlots - 1) * nb) && oe > sh_p0)
-                             ? div_nb(oe - sh_p0 + nb - 1) : 0;
-            }
             S.f0 = sh_f0;
             S.fa0 = sh_fa0;
             S.nfz = sh_nfz;
@@ -1035,7 +1034,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 done = !bfs_open && i > rho - 1;
                 publish();
                 if (dbg) dslot[8] = gtimer();
-            });
+            }, true);
             ++iters;
         }
 
