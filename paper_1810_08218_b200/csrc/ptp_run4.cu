@@ -277,10 +277,6 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     const bool exp = expand && is_new;
     ca_claim = false;
     cb_claim = false;
-    if (exp) {
-        if (hasa) ca_claim = atomicCAS(level + ida, -1, kk + 1) == -1;
-        if (hasb) cb_claim = atomicCAS(level + idb, -1, kk + 1) == -1;
-    }
     T tv = inf;
     int lv = -1;
     T ta = inf, tb = inf;
@@ -311,6 +307,12 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
             tb = ldcg(dp + idb);
             if (LABELS) lb_ = ldcg(lp + idb);
         }
+    }
+    // BFS claims (toplesets.cpp:44-52), issued after the distance loads: an atomic
+    // ahead of them in the memory pipeline would delay the loads
+    if (exp) {
+        if (hasa) ca_claim = atomicCAS(level + ida, -1, kk + 1) == -1;
+        if (hasb) cb_claim = atomicCAS(level + idb, -1, kk + 1) == -1;
     }
     if (tdbg) tdbg[5] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv)));
     if (kdbg) kdbg[13] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv))) - k0;
