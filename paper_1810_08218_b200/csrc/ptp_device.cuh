@@ -164,7 +164,7 @@ __device__ __forceinline__ unsigned long long cyc() {
 }
 // [0] start [1] work end [2] release (globaltimer); [3..6] thread-0 task stages,
 // [7] task-loop end, [8..11] barrier3 phases (clock64)
-constexpr int kDbgSlots = 16;  // v4: [11..15] stages of the first kind-2 task
+constexpr int kDbgSlots = 20;  // v4: [9..17] stages of the first newest-topleset task
 
 __device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }

@@ -71,3 +71,6 @@ if t.shape[2] >= 16:
         m = kd[ok].mean(0)
         print("first new-topleset task (ns): entry@%.0f  pv +%.0f  row +%.0f  dist +%.0f  candidates +%.0f  cas +%.0f  loop-end@%.0f" % (
             m[1], m[2], m[3], m[4], m[5], m[6], m[0]))
+        if t.shape[2] >= 17:
+            r = t[:, :, 16][ok].astype(np.float64) / 1.965
+            print("   relax4 returned @%.0f (from iteration start)" % r.mean())
