@@ -243,7 +243,8 @@ def main():
 
     # end to end through the public API (host buffers, H2D source + D2H distances)
     e2e_s = []
-    out = np.empty(n, np.float64)
+    # result lands in pinned host memory (the D2H copy runs at full PCIe/C2C speed)
+    out = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
     barrier()
     for s in range(args.steps):
         flush.zero_()
@@ -282,7 +283,9 @@ def main():
             "iterations": [x["iterations"] for x in stats][:3],
             "rho": stats[0]["rho"], "U_per_field": U / args.steps, "C_per_field": Cc / args.steps,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 4,
-                    "d2h_bytes_per_step": 8 * n, "api": "paper_1810_08218_b200.geodesics"},
+                    "d2h_bytes_per_step": 8 * n, "api": "paper_1810_08218_b200.geodesics",
+                    "host_buffers": "source list in host memory, float64 distances into a "
+                                    "pinned host array"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -128,9 +128,11 @@ struct Workspace {
     // evict the distance and level lines of the vertices the wavefront reaches next.
     char* hot = nullptr;
     size_t hot_bytes = 0;
+    mutable cudaStream_t persisted_on = nullptr;  // stream whose window covers `hot`
 
     void release() {
         if (hot) cudaFree(hot);
+        persisted_on = nullptr;
         for (void* p : {static_cast<void*>(limits), static_cast<void*>(ctl),
                         static_cast<void*>(scratch), static_cast<void*>(pring), pL, pquad,
                         static_cast<void*>(blk_slot), static_cast<void*>(blists)})
@@ -177,7 +179,7 @@ struct Workspace {
             const char* e = getenv("GEODIST_PERSIST");
             return !(e && e[0] == '0');
         }();
-        if (!on || !hot) return;
+        if (!on || !hot || persisted_on == st) return;  // set once per stream and block
         int max_persist = 0, max_window = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
@@ -196,6 +198,7 @@ struct Workspace {
         v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
         cudaGetLastError();  // the window is a hint: never fail a solve over it
+        persisted_on = st;
     }
 
     void fill(RunArgs& a) const {
