@@ -245,6 +245,8 @@ def main():
     e2e_s = []
     # result lands in pinned host memory (the D2H copy runs at full PCIe/C2C speed)
     out = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    for s in range(args.warmup):  # untimed: first calls size the API's device buffers
+        g.geodesics(mesh, [source_for(rank, s + 1000, n)], precision=args.precision, out=out)
     barrier()
     for s in range(args.steps):
         flush.zero_()
