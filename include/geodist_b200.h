@@ -191,7 +191,10 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
  * Results land in DEVICE memory of the mesh's device: out_dist (nq*n values
  * of the run precision: float for SINGLE, double for DOUBLE), out_labels
  * (nq*n int32, or NULL), out_stats (nq rows, host).  `groups` queries run
- * concurrently inside one persistent launch (0 = auto).  `stream` is a
+ * concurrently inside one persistent launch; 0 = auto: query 0 runs on the whole
+ * GPU and its mean band per CTA picks 1..8 groups for the rest (narrow,
+ * latency-bound fields gain from concurrency, wide ones do not); wall_seconds
+ * of every row is then the device time of both launches.  `stream` is a
  * cudaStream_t (NULL = the mesh's own stream); the call returns after the
  * launch completes. */
 int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int32_t* offsets,

@@ -961,6 +961,38 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
                          int32_t nq, const geodist_ptp_config* config, void* out_dist,
                          int32_t* out_labels, geodist_ptp_stats* out_stats, int32_t groups,
                          void* stream) {
+    if (groups <= 0 && nq >= 3 && mesh && config && sources && offsets && out_dist) {
+        // Automatic grouping: query 0 runs on the whole GPU; its mean band per CTA
+        // tells whether fields here are latency-bound (narrow bands: many concurrent
+        // groups raise throughput, measured 2x at 8 groups on the icosphere-8) or
+        // throughput-bound (wide bands: one group is fastest, e.g. the 1000^2 torus).
+        geodist_ptp_stats s0{};
+        int rc = geodist_batch_device(mesh, sources, offsets, 1, config, out_dist, out_labels,
+                                      &s0, 1, stream);
+        if (rc != GEODIST_OK) return rc;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, M(mesh)->device);
+        const double band = s0.iterations > 0 ? double(s0.vertex_updates) / s0.iterations : 0.0;
+        const double per_cta = band / std::max(1, sms);
+        const int g = per_cta < 160 ? 8 : per_cta < 400 ? 4 : per_cta < 800 ? 2 : 1;
+        std::vector<int32_t> off(nq);
+        for (int q = 1; q <= nq - 1; ++q) off[q - 1] = offsets[q] - offsets[1];
+        off[nq - 1] = offsets[nq] - offsets[1];
+        const size_t n = M(mesh)->n;
+        const size_t esz = config->precision == GEODIST_DOUBLE ? 8 : 4;
+        std::vector<geodist_ptp_stats> rest(nq - 1);
+        rc = geodist_batch_device(mesh, sources + offsets[1], off.data(), nq - 1, config,
+                                  static_cast<char*>(out_dist) + n * esz,
+                                  out_labels ? out_labels + n : nullptr, rest.data(), g, stream);
+        if (rc != GEODIST_OK) return rc;
+        if (out_stats) {
+            const double total = s0.wall_seconds + rest[0].wall_seconds;
+            out_stats[0] = s0;
+            for (int q = 1; q < nq; ++q) out_stats[q] = rest[q - 1];
+            for (int q = 0; q < nq; ++q) out_stats[q].wall_seconds = out_stats[q].total_seconds = total;
+        }
+        return GEODIST_OK;
+    }
     return guarded([&] {
         auto* mh = M(mesh);
         std::lock_guard<std::mutex> lock(mh->mu);
