@@ -32,11 +32,11 @@ if "ico8" in which:
 if "torus" in which:
     M = g.generate_torus(1000, 1000)
     out["torus1000"] = {p: field(M, [0], p, reps=2) for p in ("single", "double")}
-if "height" in which:
+if "height" in which or "height64" in which:
     M = g.heightfield_grid(2048, 2048)
     src = [((2 * b + 1) * 256) * 2048 + (2 * a + 1) * 256 for b in range(4) for a in range(4)]
-    out["height2048_16src_labels"] = {p: field(M, src, p, labels=True, reps=1)
-                                      for p in ("single",)}
+    precs = ("single",) if "height64" not in which else ("single", "double")
+    out["height2048_16src_labels"] = {p: field(M, src, p, labels=True, reps=1) for p in precs}
 if "fps" in which:
     M = g.generate_torus(1000, 1000)
     t = time.perf_counter()
