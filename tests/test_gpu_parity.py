@@ -149,6 +149,8 @@ def polar_arrays(spokes, rings, twist=0.37):
 SYNTH = [
     ("wheel12", lambda: polar_arrays(12, 9), [[0], [5, 40]]),
     ("wheel23", lambda: polar_arrays(23, 6), [[0], [3]]),
+    # 5000 claims by one CTA in one iteration: the on-chip claim list spills to global
+    ("wheel5000", lambda: polar_arrays(5000, 3), [[0], [7, 12000]]),
     ("ico5", lambda: g.icosphere_arrays(5), [[0], [5, 700, 9000]]),
     ("noisy_ico6", lambda: g.noisy_icosphere_arrays(6, 2e-3, 1), [[0], [1, 20000, 33333, 40000]]),
     ("torus64x48", lambda: g.torus_arrays(64, 48), [[0], [17, 1500, 3000]]),
