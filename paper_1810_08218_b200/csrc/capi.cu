@@ -469,11 +469,17 @@ void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
     std::vector<double> snap;
     float total_ms = 0.f;
     GroupCtl hctl{};
+    // v4 without per-iteration host work: the narrow-band and wide-band
+    // instantiations hand the field to each other at band cross-overs (each
+    // carries only its own path's registers); otherwise the combined kernel.
+    const bool switching = version == 4 && chunk <= 0 && !getenv("GEODIST_NO_MODES");
+    int launch_version = switching ? 5 : version;
     for (int launch = 0;; ++launch) {
         a.phase_init = launch == 0 ? 1 : 0;
         a.trace_k0 = hctl.k + 1;
+        if (switching && launch >= 64) launch_version = 4;  // pathological oscillation
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
-        cuda_ok(launch_run(prec, labels, a, st, version), "ptp_run_kernel launch");
+        cuda_ok(launch_run(prec, labels, a, st, launch_version), "ptp_run_kernel launch");
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         cuda_ok(cudaMemcpyAsync(&hctl, ws.ctl, sizeof(GroupCtl), cudaMemcpyDeviceToHost, st),
                 "read state");
@@ -500,6 +506,10 @@ void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
             q.observer(q.observer_user, hctl.k, snap.data(), n);
         }
         if (hctl.done) break;
+        if (switching && hctl.mode_exit != 0) {
+            launch_version = hctl.mode_exit == 2 ? 6 : 5;
+            continue;
+        }
         if (chunk <= 0) throw Fail(GEODIST_ECUDA, "solver returned before convergence");
     }
     QueryStats qs{};

@@ -51,7 +51,7 @@ struct alignas(128) GroupCtl {
     int err;
     int pad2[30];
     // loop state, saved by CTA 0 of the group when a launch ends mid-run
-    int k, i, rho, parity, retired, bfs_open, done, initialized;
+    int k, i, rho, parity, mode_exit, bfs_open, done, initialized;  // mode_exit: v4 kernel to resume with
     int s_tail, s_limk, s_bb, s_fe, s_frzb, s_frze, pad3[2];
     unsigned long long relax, degen, updates;
     unsigned long long pad4[5];
@@ -138,6 +138,7 @@ struct RunArgs {
     int* blists;         // [2][gridDim.x][claim_cap] per-CTA claim lists
     int claim_cap;       // capacity of one claim list
     int cache_slots;     // v4: shared-memory record cache slots per CTA
+    int mode;            // v4 launch mode: 0 combined, 1 narrow bands only, 2 wide bands only
 };
 
 // Per-CTA barrier payload slot (16 B): max relative change bits and claims.

@@ -1472,7 +1472,7 @@ __global__ void reset_bars_kernel(GroupCtl* ctl, int groups) {
 }
 
 static const void* run_kernel_ptr(int version, int precision, bool labels) {
-    if (version == 4) return run4_kernel_ptr(precision, labels);
+    if (version >= 4) return run4_kernel_ptr(precision, labels, version - 4);
     if (version == 2) {
         if (precision == 0)
             return labels ? reinterpret_cast<const void*>(&ptp_run_kernel<float, true>)
@@ -1489,7 +1489,7 @@ static const void* run_kernel_ptr(int version, int precision, bool labels) {
 
 // v4: shared-memory record cache
 static size_t run_dyn_smem(int version, int precision, bool labels) {
-    return version == 4 ? run4_dyn_smem(precision, labels) : 0;
+    return version >= 4 ? run4_dyn_smem(precision, labels) : 0;
 }
 
 int run_max_blocks(int precision, bool labels, int device, int version) {

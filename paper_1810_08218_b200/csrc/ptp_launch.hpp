@@ -24,7 +24,7 @@ void launch_planar_test(int precision, const double* x1, const double* x2, const
 int run_max_blocks(int precision, bool labels, int device, int version = 3);
 // v4 (ptp_run4.cu): record-cache bytes (dynamic shared memory) and kernel entry
 size_t run4_dyn_smem(int precision, bool labels);
-const void* run4_kernel_ptr(int precision, bool labels);
+const void* run4_kernel_ptr(int precision, bool labels, int mode = 0);
 cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st,
                        int version = 3);
 

@@ -553,7 +553,11 @@ __device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, i
 
 }  // namespace
 
-template <typename T, bool LABELS>
+// MODE 0: every iteration (narrow bands through the record cache, wide ones one
+// vertex per thread); MODE 1: narrow iterations only, MODE 2: wide only -- each
+// exits (state saved in GroupCtl, mode_exit = the other mode) when the band
+// crosses over, so each instantiation carries only its own path's registers.
+template <typename T, bool LABELS, int MODE>
 __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ Bcast4 S;
@@ -848,13 +852,18 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 __syncthreads();
             }
         } else {
-            // resume a run stopped by max_iters: state from ctl, limits from global
+            // resume a run stopped by max_iters or a mode switch: state from ctl, the
+            // limits ring reloaded from global memory
+            const int top = ctl->bfs_open ? ctl->k + 2 : ctl->rho;
+            const int lo = top - kLimRing + 1 > 0 ? top - kLimRing + 1 : 0;
+            for (int r = lo + tid; r <= top; r += kBlock) s_lim[r % kLimRing] = ldcg(limits + r);
+            __syncthreads();
             if (tid == 0) {
                 k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
                 bfs_open = ctl->bfs_open; done = ctl->done;
                 tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
                 frzb = ctl->s_frzb; frze = ctl->s_frze;
-                use_glim = true;
+                lim_top = top;
                 shares_now();
                 publish();
             }
@@ -863,8 +872,21 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
 
         long long calls = 0, degs = 0;
         int iters = 0;
+        int mode_exit = 0;
         for (;;) {
             if (S.done || (A.max_iters > 0 && iters >= A.max_iters)) break;
+            if constexpr (MODE != 0) {
+                const int span = S.be - S.bb;
+                const bool wide = A.wide_factor == 0 || span > (kCacheSlots - 1) * nb;
+                if (MODE == 1 && wide) {
+                    mode_exit = 2;
+                    break;
+                }
+                if (MODE == 2 && A.wide_factor != 0 && 2 * span <= (kCacheSlots - 1) * nb) {
+                    mode_exit = 1;  // narrow again (with hysteresis)
+                    break;
+                }
+            }
             const int kk = S.k;
             const bool dbg = A.dbg != nullptr && tid == 0 && iters < A.dbg_iters;
             unsigned long long* dslot =
@@ -879,7 +901,9 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             const int bb_ = S.bb, be_ = S.be, fe_ = S.fe, oe_ = S.oe;
             const bool expand = S.expand != 0;
             // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
-            const bool cached = A.wide_factor != 0 && (be_ - bb_) <= (kCacheSlots - 1) * nb;
+            const bool cached = MODE == 1   ? true
+                                : MODE == 2 ? false
+                                            : A.wide_factor != 0 && (be_ - bb_) <= (kCacheSlots - 1) * nb;
             const bool pack = !cached || 2 * (be_ - bb_) > (kCacheSlots - 1) * nb;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
@@ -1050,6 +1074,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if (lb == 0) {
                 ctl->k = k; ctl->i = i; ctl->rho = rho; ctl->parity = parity;
                 ctl->bfs_open = bfs_open; ctl->done = done;
+                ctl->mode_exit = mode_exit;
                 ctl->s_tail = tail; ctl->s_limk = limk; ctl->s_bb = bb; ctl->s_fe = fe;
                 ctl->s_frzb = frzb; ctl->s_frze = frze;
                 ctl->updates += upd;
@@ -1149,12 +1174,17 @@ size_t run4_dyn_smem(int precision, bool) {
            (precision == 0 ? Cache<float>::bytes_per_slot() : Cache<double>::bytes_per_slot());
 }
 
-const void* run4_kernel_ptr(int precision, bool labels) {
+template <int MODE> static const void* run4_ptr(int precision, bool labels) {
     if (precision == 0)
-        return labels ? reinterpret_cast<const void*>(&ptp_run4_kernel<float, true>)
-                      : reinterpret_cast<const void*>(&ptp_run4_kernel<float, false>);
-    return labels ? reinterpret_cast<const void*>(&ptp_run4_kernel<double, true>)
-                  : reinterpret_cast<const void*>(&ptp_run4_kernel<double, false>);
+        return labels ? reinterpret_cast<const void*>(&ptp_run4_kernel<float, true, MODE>)
+                      : reinterpret_cast<const void*>(&ptp_run4_kernel<float, false, MODE>);
+    return labels ? reinterpret_cast<const void*>(&ptp_run4_kernel<double, true, MODE>)
+                  : reinterpret_cast<const void*>(&ptp_run4_kernel<double, false, MODE>);
+}
+
+const void* run4_kernel_ptr(int precision, bool labels, int mode) {
+    return mode == 1 ? run4_ptr<1>(precision, labels)
+                     : mode == 2 ? run4_ptr<2>(precision, labels) : run4_ptr<0>(precision, labels);
 }
 
 }  // namespace gdb
