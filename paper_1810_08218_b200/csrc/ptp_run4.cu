@@ -421,36 +421,58 @@ template <> __device__ __forceinline__ void load_L8_cg<double>(const double* bas
     L[2] = c.x; L[6] = c.y; L[3] = d.x; L[7] = d.y;
 }
 
-template <typename T, bool LABELS>
-__device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A, int p, int kk,
-                                           const int* pv, const int* pring, const T* pL,
-                                           const char* pquad, const T* dp, T* dc, const int* lp,
-                                           int* lc, int fe, T eps, int& nonconv, T& my_max,
-                                           long long& calls, long long& degs) {
-    const T inf = Lim<T>::inf();
-    const int vr = ldcg(pv + p);
-    const int v = vr & kIdMask;
+// The record half of a wide task, loaded one task ahead (wide_load) so that its
+// trips overlap the previous task's relaxation (relax_wide).
+template <typename T> struct WideRec {
+    int p, vr;
+    int raw[kEllW];
+    T L[kEllW];
+};
+
+template <typename T>
+__device__ __forceinline__ void wide_load(const MeshDev& M, const RunArgs& A, int p,
+                                          const int* pv, const int* pring, const T* pL,
+                                          WideRec<T>& r) {
+    r.p = p;
+    r.vr = ldcg(pv + p);
+    const int v = r.vr & kIdMask;
     // packed records are slot-major (slot s of position p at s * N + p): a warp on 32
     // consecutive positions reads each slot as one contiguous run
     size_t pb = static_cast<size_t>(p), step = static_cast<size_t>(A.stride);
     const int* rsrc = pring;
     const T* lsrc = pL;
-    const char* qsrc = pquad;
-    if (!(vr & kPacked)) {
+    if (!(r.vr & kPacked)) {
         // no packed record (the vertex entered the band while it was narrow): ELL by id
         pb = static_cast<size_t>(v) * kEllW;
         step = 1;
         rsrc = M.ering;
         lsrc = static_cast<const T*>(M.eL);
-        qsrc = static_cast<const char*>(M.equad);
     }
-    int raw[kEllW];
-    T L[kEllW];
 #pragma unroll
     for (int e = 0; e < kEllW; ++e) {
-        raw[e] = __ldcg(rsrc + pb + ell_slot(e) * step);
-        L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
+        r.raw[e] = __ldcg(rsrc + pb + ell_slot(e) * step);
+        r.L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
     }
+}
+
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A,
+                                           const WideRec<T>& rec, int kk, const char* pquad,
+                                           const T* dp, T* dc, const int* lp, int* lc, int fe,
+                                           T eps, int& nonconv, T& my_max, long long& calls,
+                                           long long& degs) {
+    const T inf = Lim<T>::inf();
+    const int p = rec.p;
+    const int v = rec.vr & kIdMask;
+    size_t pb = static_cast<size_t>(p), step = static_cast<size_t>(A.stride);
+    const char* qsrc = pquad;
+    if (!(rec.vr & kPacked)) {
+        pb = static_cast<size_t>(v) * kEllW;
+        step = 1;
+        qsrc = static_cast<const char*>(M.equad);
+    }
+    const int* raw = rec.raw;
+    const T* L = rec.L;
     const T tv = ldcg(dp + v);
     const int lv = LABELS ? ldcg(lp + v) : -1;
     int d = (raw[0] >> kMetaShift) & 15;
@@ -915,7 +937,9 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             // wide iterations (band beyond the record cache, fp32): the generic loop takes
             // only the newest topleset; older positions are relaxed one per thread below
             // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
-            constexpr bool kThreadWide = sizeof(T) == 4;
+            // (the wide-only instantiation has no narrow path to protect: fp64 too, but
+            // not fp64 with labels, whose per-thread fan spills)
+            constexpr bool kThreadWide = sizeof(T) == 4 || (MODE == 2 && !LABELS);
             // Wide iterations (fp32): positions are dealt to CTAs in chunks of 32
             // consecutive positions (chunk c -> CTA c mod nb) instead of one by one, so
             // a warp works on 32 neighbouring positions: their records are adjacent and,
@@ -988,14 +1012,20 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     if (LABELS) lc[v] = ldcg(lp + v);
                 }
             }
-            if (kThreadWide) {
+            if constexpr (kThreadWide) {
                 // older band positions [bb, oe): one vertex per thread, chunked
-                for (int t = tid;; t += kBlock) {
-                    const int p = bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
-                    if (p - (t % kChunk) >= oe_) break;
-                    if (p < oe_)
-                        relax_wide<T, LABELS>(M, A, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc,
-                                              fe_, eps, nonconv, my_max, calls, degs);
+                auto pos = [&](int t) { return bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk); };
+                {
+                    for (int t = tid;; t += kBlock) {
+                        const int p = pos(t);
+                        if (p - (t % kChunk) >= oe_) break;
+                        if (p < oe_) {
+                            WideRec<T> rec;
+                            wide_load<T>(M, A, p, pv, pring, pL, rec);
+                            relax_wide<T, LABELS>(M, A, rec, kk, pquad, dp, dcur, lp, lc, fe_,
+                                                  eps, nonconv, my_max, calls, degs);
+                        }
+                    }
                 }
             }
             }
