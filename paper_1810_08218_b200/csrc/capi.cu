@@ -930,7 +930,20 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
             a.fps_final = s == count;
             a.out_labels = s == count ? static_cast<int*>(lab.get()) : nullptr;
             a.qstats = static_cast<QueryStats*>(hist.get()) + (s - 1);
-            cuda_ok(launch_run(prec, s > 1, a, st, version), "fps round launch");
+            if (version == 4) {
+                // no host round trip between rounds: a fixed launch sequence per round,
+                // narrow-only -> wide-only -> narrow-only -> combined, each resuming the
+                // field where the previous one handed it over (a launch whose field is
+                // complete returns at once)
+                for (int x = 0; x < 4; ++x) {
+                    a.phase_init = x == 0 ? 1 : 0;
+                    const int v = x == 3 ? 4 : (x & 1) ? 6 : 5;
+                    cuda_ok(launch_run(prec, s > 1, a, st, v), "fps round launch");
+                }
+                a.phase_init = 1;
+            } else {
+                cuda_ok(launch_run(prec, s > 1, a, st, version), "fps round launch");
+            }
         }
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         cuda_ok(cudaStreamSynchronize(st), "fps");

@@ -875,7 +875,10 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             }
         } else {
             // resume a run stopped by max_iters or a mode switch: state from ctl, the
-            // limits ring reloaded from global memory
+            // limits ring reloaded from global memory.  A launch of a fixed launch
+            // sequence (FPS rounds, batched fields) whose field is already complete
+            // has nothing to do (every CTA reads the same ctl).
+            if (__ldcg(&ctl->done)) return;
             const int top = ctl->bfs_open ? ctl->k + 2 : ctl->rho;
             const int lo = top - kLimRing + 1 > 0 ? top - kLimRing + 1 : 0;
             for (int r = lo + tid; r <= top; r += kBlock) s_lim[r % kLimRing] = ldcg(limits + r);
