@@ -1073,7 +1073,26 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         a.out_labels = config->with_labels ? out_labels : nullptr;
         a.qstats = static_cast<QueryStats*>(qs.get());
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
-        cuda_ok(launch_run(prec, multi, a, st, version), "batch launch");
+        if (version == 4 && g == 1) {
+            // one field at a time on the whole GPU (wide-band meshes): the narrow/wide
+            // launch sequence per query, enqueued without host round trips
+            const size_t esz = prec == GEODIST_DOUBLE ? 8 : 4;
+            for (int q = 0; q < nq; ++q) {
+                a.nq = 1;
+                a.src_off = static_cast<int*>(offb.get()) + q;
+                a.out_dist = static_cast<char*>(out_dist) + static_cast<size_t>(q) * n * esz;
+                a.out_labels = config->with_labels && out_labels ? out_labels + static_cast<size_t>(q) * n
+                                                                 : nullptr;
+                a.qstats = static_cast<QueryStats*>(qs.get()) + q;
+                for (int x = 0; x < 4; ++x) {
+                    a.phase_init = x == 0 ? 1 : 0;
+                    const int v = x == 3 ? 4 : (x & 1) ? 6 : 5;
+                    cuda_ok(launch_run(prec, multi, a, st, v), "batch launch");
+                }
+            }
+        } else {
+            cuda_ok(launch_run(prec, multi, a, st, version), "batch launch");
+        }
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         std::vector<QueryStats> hq(nq);
         cuda_ok(cudaMemcpyAsync(hq.data(), qs.get(), sizeof(QueryStats) * nq,
