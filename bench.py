@@ -189,9 +189,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for the multi-rank path on a one-GPU box: every rank on one device,
+    # gloo instead of NCCL (collectives then run on host copies)
+    if os.environ.get("BENCH_FORCE_DEVICE"):
+        local = int(os.environ["BENCH_FORCE_DEVICE"])
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def coll(t):  # tensor as the process group's backend wants it
+        return t if backend == "nccl" else t.cpu()
 
     V, F = workload_arrays()
     n = len(V)
@@ -223,11 +234,13 @@ def main():
             dev_s.append(st["device_seconds"])
             stats.append(st)
         if world > 1:
-            gathered = [torch.empty_like(results) for _ in range(world)] if rank == 0 else None
+            # per-query results gathered to rank 0 (the only collective: SURVEY 8e)
+            res = coll(results)
+            gathered = [torch.empty_like(res) for _ in range(world)] if rank == 0 else None
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record()
-            dist.gather(results, gathered, dst=0)
+            dist.gather(res, gathered, dst=0)
             t1.record()
             torch.cuda.synchronize()
             dev_s.append(t0.elapsed_time(t1) * 1e-3)
@@ -235,7 +248,7 @@ def main():
     launches = g._capi.kernel_launches() - launches0
     total = sum(dev_s)
     if world > 1:
-        tt = torch.tensor([total], dtype=torch.float64, device="cuda")
+        tt = coll(torch.tensor([total], dtype=torch.float64, device="cuda"))
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total = float(tt.item())
     ms_field = 1e3 * total / (world * args.steps)
@@ -257,7 +270,7 @@ def main():
     barrier()
     e2e_total = sum(e2e_s)
     if world > 1:
-        tt = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+        tt = coll(torch.tensor([e2e_total], dtype=torch.float64, device="cuda"))
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_total = float(tt.item())
     e2e_ms = 1e3 * e2e_total / (world * args.steps)
