@@ -103,8 +103,10 @@ int geodist_device_count(int32_t* count);
 
 /* ---- meshes ---------------------------------------------------------- */
 /* Validates (validate_mesh, mesh.cpp:11-34), builds the rotational fans
- * (build_connectivity, connectivity.cpp:19-81) and uploads the fan-CSR to
- * `device`.  xyz: n*3 doubles, faces: nf*3 int32.  xyz may be NULL for a
+ * (build_connectivity, connectivity.cpp:19-81) and keeps the fan-CSR on
+ * `device`.  The build runs on the device from the uploaded faces
+ * (GEODIST_HOST_BUILD=1 selects the host build); a rejected mesh reports the
+ * reference's error text.  xyz: n*3 doubles, faces: nf*3 int32.  xyz may be NULL for a
  * topology-only mesh (toplesets / reorder only; compute_toplesets receives a
  * Connectivity without positions). */
 int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int32_t nf,
@@ -117,6 +119,9 @@ int geodist_mesh_degrees(geodist_mesh_t mesh, int32_t* degree);
  * returns the corner count in *count (needs cap >= count). */
 int geodist_mesh_fan(geodist_mesh_t mesh, int32_t v, int32_t* v1, int32_t* v2, int32_t cap,
                      int32_t* count);
+/* The whole fan-CSR of a mesh (the layout of geodist_build_fans): cptr n+1,
+ * ring 3*nf + n, degree n; any pointer may be NULL. */
+int geodist_mesh_fans(geodist_mesh_t mesh, int32_t* cptr, int32_t* ring, int32_t* degree);
 
 /* Host-only fan build (no device): validation + rotational fans exactly as
  * geodist_mesh_create computes them.  cptr: n+1; ring: 3*nf + n entries

@@ -87,6 +87,16 @@ class Mesh:
         check(lib().geodist_mesh_fan(self._h, int(v), a, b, cap, C.byref(cnt)))
         return a[:cnt.value].copy(), b[:cnt.value].copy()
 
+    def fans(self):
+        """The mesh's fan-CSR as built (on the device): (cptr[n+1], ring[3F+n], degree[n]),
+        the layout of :func:`build_fans`."""
+        n = self.n_vertices
+        cptr = np.empty(n + 1, np.int32)
+        ring = np.empty(3 * self.n_faces + n + 1, np.int32)
+        deg = np.empty(max(n, 1), np.int32)
+        check(lib().geodist_mesh_fans(self._h, cptr, ring, deg))
+        return cptr, ring[:cptr[n] + n], deg[:n]
+
     def __repr__(self):
         return f"<geodist.Mesh with {self.n_vertices} vertices, {self.n_faces} faces>"
 

@@ -18,6 +18,7 @@ GEODIST_OK, GEODIST_EINVAL, GEODIST_EMESH, GEODIST_ECUDA, GEODIST_ENOMEM = range
 EXPORTED = [
     "geodist_last_error", "geodist_version", "geodist_device_count", "geodist_mesh_create",
     "geodist_mesh_destroy", "geodist_mesh_sizes", "geodist_mesh_degrees", "geodist_mesh_fan",
+    "geodist_mesh_fans",
     "geodist_build_fans", "geodist_validate_mesh", "geodist_build_halfedges", "geodist_grid_sizes", "geodist_generate_grid", "geodist_icosphere_sizes",
     "geodist_generate_icosphere", "geodist_perturb_radial", "geodist_torus_sizes",
     "geodist_generate_torus", "geodist_heightfield", "geodist_toplesets",
@@ -79,6 +80,7 @@ def lib():
         L.geodist_mesh_degrees.argtypes = [_vp, _i32p]
         L.geodist_mesh_fan.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.c_int32,
                                        C.POINTER(C.c_int32)]
+        L.geodist_mesh_fans.argtypes = [_vp, _i32p, _i32p, _i32p]
         L.geodist_build_fans.argtypes = [_f64p, C.c_int32, _i32p, C.c_int32, _i32p, _i32p, _vp]
         L.geodist_validate_mesh.argtypes = [_f64p, C.c_int32, _i32p, C.c_int32]
         L.geodist_build_halfedges.argtypes = [_vp, C.c_int32, _i32p, C.c_int32, _i32p, _i32p]

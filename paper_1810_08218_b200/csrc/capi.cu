@@ -239,7 +239,10 @@ struct geodist_mesh_s {
     int device = 0;
     int n = 0, nf = 0;
     long long corners = 0;
-    Fans fans;
+    Fans fans;               // host copy of the fan-CSR, downloaded on first use
+    bool host_fans = false;  // (vertex_star / degree queries only; the solver never needs it)
+    std::mutex fans_mu;
+    int* degree_d = nullptr;
     double* xyz = nullptr;
     int* faces = nullptr;
     int* cptr = nullptr;
@@ -278,7 +281,7 @@ struct geodist_mesh_s {
                         static_cast<void*>(cptr), static_cast<void*>(ring),
                         static_cast<void*>(t_sorted), static_cast<void*>(t_position),
                         static_cast<void*>(t_scratch), static_cast<void*>(d_src),
-                        static_cast<void*>(d_i32)})
+                        static_cast<void*>(d_i32), static_cast<void*>(degree_d)})
             if (p) cudaFree(p);
         for (auto& t : prec)
             for (void* p : {static_cast<void*>(t.ring), t.ringL, t.quad,
@@ -335,6 +338,27 @@ namespace {
 geodist_mesh_s* M(geodist_mesh_t h) {
     if (!h) throw Fail(GEODIST_EINVAL, "null mesh handle");
     return static_cast<geodist_mesh_s*>(h);
+}
+
+// Host copy of a device-built fan-CSR (downloaded once, on the first host-side query).
+const Fans& host_fans(geodist_mesh_s* m) {
+    std::lock_guard<std::mutex> lk(m->fans_mu);
+    if (m->host_fans) return m->fans;
+    cuda_ok(cudaSetDevice(m->device), "cudaSetDevice");
+    Fans& f = m->fans;
+    f.n = m->n;
+    f.cptr.resize(static_cast<size_t>(m->n) + 1);
+    f.ring.resize(static_cast<size_t>(m->corners) + m->n);
+    f.degree.resize(static_cast<size_t>(m->n));
+    cuda_ok(cudaMemcpy(f.cptr.data(), m->cptr, sizeof(int) * f.cptr.size(), cudaMemcpyDeviceToHost),
+            "download fans");
+    cuda_ok(cudaMemcpy(f.ring.data(), m->ring, sizeof(int) * f.ring.size(), cudaMemcpyDeviceToHost),
+            "download fans");
+    if (m->n)
+        cuda_ok(cudaMemcpy(f.degree.data(), m->degree_d, sizeof(int) * f.degree.size(),
+                           cudaMemcpyDeviceToHost), "download fans");
+    m->host_fans = true;
+    return f;
 }
 
 // compute_toplesets source validation (toplesets.cpp:18-34): sorted copy.
@@ -590,21 +614,31 @@ int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int3
         *out = nullptr;
         if (n < 0 || nf < 0 || (nf > 0 && !faces))
             throw Fail(GEODIST_EINVAL, "invalid mesh arrays");
-        Fans fans = build_fans(xyz, n, faces, nf);  // runtime_error -> EMESH
+        int count = 0;
+        const bool have_gpu = cudaGetDeviceCount(&count) == cudaSuccess && count > 0;
+        if (!have_gpu) cudaGetLastError();
+        // The fan-CSR is built on the device (mesh_build.cu); the host build runs only
+        // when asked for (GEODIST_HOST_BUILD=1), for meshes beyond int32 half-edge ids,
+        // and -- for its exact error text -- on a mesh the device build rejects or on a
+        // machine without a device (mesh errors before device errors, as before).
+        const char* hb = std::getenv("GEODIST_HOST_BUILD");
+        const bool host_build = !have_gpu || (hb && hb[0] == '1') || 3LL * nf > INT32_MAX;
+        Fans fans;
+        if (host_build) fans = build_fans(xyz, n, faces, nf);  // runtime_error -> EMESH
         if (n > kIdMask) throw Fail(GEODIST_EINVAL, "mesh too large: at most 2^27-1 vertices");
         require_device(device);
         std::unique_ptr<geodist_mesh_s> m(new geodist_mesh_s);
         m->device = device;
         m->n = n;
         m->nf = nf;
-        m->corners = fans.cptr[n];
+        m->corners = 3LL * nf;  // every outgoing half-edge of a manifold star is a corner
         cuda_ok(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
         cuda_ok(cudaEventCreate(&m->ev0), "event");
         cuda_ok(cudaEventCreate(&m->ev1), "event");
         m->xyz = dalloc<double>(3 * static_cast<size_t>(n));
         m->faces = dalloc<int>(3 * static_cast<size_t>(nf));
         m->cptr = dalloc<int>(static_cast<size_t>(n) + 1);
-        m->ring = dalloc<int>(fans.ring.size());
+        m->ring = dalloc<int>(3 * static_cast<size_t>(nf) + n);
         m->has_geometry = xyz != nullptr;
         if (xyz)
             cuda_ok(cudaMemcpy(m->xyz, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice),
@@ -612,11 +646,31 @@ int geodist_mesh_create(const double* xyz, int32_t n, const int32_t* faces, int3
         if (nf)
             cuda_ok(cudaMemcpy(m->faces, faces, sizeof(int) * 3 * nf, cudaMemcpyHostToDevice),
                     "upload");
-        cuda_ok(cudaMemcpy(m->cptr, fans.cptr.data(), sizeof(int) * (n + 1),
-                           cudaMemcpyHostToDevice), "upload");
-        cuda_ok(cudaMemcpy(m->ring, fans.ring.data(), sizeof(int) * fans.ring.size(),
-                           cudaMemcpyHostToDevice), "upload");
-        m->fans = std::move(fans);
+        if (host_build) {
+            cuda_ok(cudaMemcpy(m->cptr, fans.cptr.data(), sizeof(int) * (n + 1),
+                               cudaMemcpyHostToDevice), "upload");
+            cuda_ok(cudaMemcpy(m->ring, fans.ring.data(), sizeof(int) * fans.ring.size(),
+                               cudaMemcpyHostToDevice), "upload");
+            m->fans = std::move(fans);
+            m->host_fans = true;
+        } else {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+            m->degree_d = dalloc<int>(static_cast<size_t>(n));
+            std::unique_ptr<int, DFree> scratch(
+                dalloc<int>(build_fans_scratch_ints(n, nf) + 3 * static_cast<size_t>(nf)));
+            int* twin = scratch.get() + build_fans_scratch_ints(n, nf);
+            cudaError_t err = cudaSuccess;
+            const unsigned flag =
+                build_fans_device(xyz ? m->xyz : nullptr, n, m->faces, nf, m->cptr, m->ring,
+                                  m->degree_d, twin, scratch.get(), sms, m->stream, &err);
+            cuda_ok(err, "device mesh build");
+            if (flag) {
+                build_fans(xyz, n, faces, nf);  // throws the reference's message
+                throw std::runtime_error("mesh rejected by the device build (flags " +
+                                         std::to_string(flag) + ")");
+            }
+        }
         *out = m.release();
     });
 }
@@ -637,7 +691,8 @@ int geodist_mesh_sizes(geodist_mesh_t mesh, int32_t* n, int32_t* nf, int64_t* co
 int geodist_mesh_degrees(geodist_mesh_t mesh, int32_t* degree) {
     return guarded([&] {
         auto* m = M(mesh);
-        std::copy(m->fans.degree.begin(), m->fans.degree.end(), degree);
+        const Fans& f = host_fans(m);
+        std::copy(f.degree.begin(), f.degree.end(), degree);
     });
 }
 
@@ -646,13 +701,24 @@ int geodist_mesh_fan(geodist_mesh_t mesh, int32_t v, int32_t* v1, int32_t* v2, i
     return guarded([&] {
         auto* m = M(mesh);
         if (v < 0 || v >= m->n) throw std::invalid_argument("vertex_star: index out of range");
-        const int c0 = m->fans.cptr[v], d = m->fans.cptr[v + 1] - c0, r0 = c0 + v;
+        const Fans& f = host_fans(m);
+        const int c0 = f.cptr[v], d = f.cptr[v + 1] - c0, r0 = c0 + v;
         *count = d;
         if (d > cap) throw Fail(GEODIST_EINVAL, "fan larger than cap");
         for (int c = 0; c < d; ++c) {
-            v1[c] = m->fans.ring[r0 + c];
-            v2[c] = m->fans.ring[r0 + c + 1];
+            v1[c] = f.ring[r0 + c];
+            v2[c] = f.ring[r0 + c + 1];
         }
+    });
+}
+
+int geodist_mesh_fans(geodist_mesh_t mesh, int32_t* cptr, int32_t* ring, int32_t* degree) {
+    return guarded([&] {
+        auto* m = M(mesh);
+        const Fans& f = host_fans(m);
+        if (cptr) std::copy(f.cptr.begin(), f.cptr.end(), cptr);
+        if (ring) std::copy(f.ring.begin(), f.ring.end(), ring);
+        if (degree) std::copy(f.degree.begin(), f.degree.end(), degree);
     });
 }
 

@@ -53,4 +53,11 @@ cudaError_t launch_reorder(const int* position, const int* sorted, int reachable
                            const int* faces, int nf, int* old_of_new, int* new_of_old,
                            int* faces_out, cudaStream_t st);
 
+// On-device fan-CSR build (mesh_build.cu).  Returns 0 for a valid mesh, else the
+// validation flag bits (~0u with *err set on a CUDA error).
+size_t build_fans_scratch_ints(int n, int nf);
+unsigned build_fans_device(const double* xyz, int n, const int* faces, int nf, int* cptr,
+                           int* ring, int* degree, int* twin, int* scratch, int sms,
+                           cudaStream_t st, cudaError_t* err);
+
 }  // namespace gdb

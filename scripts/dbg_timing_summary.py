@@ -74,3 +74,18 @@ if t.shape[2] >= 16:
         if t.shape[2] >= 17:
             r = t[:, :, 16][ok].astype(np.float64) / 1.965
             print("   relax4 returned @%.0f (from iteration start)" % r.mean())
+# wide iterations (slot 18 = 1): newest topleset (4-lane groups) vs older positions
+# (one vertex per thread) vs barrier, globaltimer ns
+if t.shape[2] >= 19:
+    w = t[:, :, 18] == 1
+    wi = w.all(axis=1)
+    if wi.any():
+        tw = t[wi]
+        newest = (tw[:, :, 17] - tw[:, :, 0])
+        older = (tw[:, :, 1] - tw[:, :, 17])
+        bar = (tw[:, :, 2] - tw[:, :, 1])
+        per = tw[:, :, 2].max(1) - tw[:, :, 0].min(1)
+        print("wide iterations %d: newest-topleset part mean %.0f (max-over-CTAs %.0f), "
+              "older part mean %.0f (max %.0f), barrier mean %.0f, start->last release %.0f ns" % (
+                  wi.sum(), newest.mean(), newest.max(1).mean(), older.mean(), older.max(1).mean(),
+                  bar.mean(), per.mean()))

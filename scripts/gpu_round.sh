@@ -15,6 +15,8 @@ for P in single double; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:ptp_run4 -s 3 -c 1 -o gpurun_out/prof_${P} python bench.py --steps 1 --warmup 3 --no-cpu-baseline --precision $P > gpurun_out/ncu_${P}.log 2>&1
   tail -1 gpurun_out/ncu_${P}.log
 done
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:ptp_run4 -s 1 -c 1 -o gpurun_out/prof_torus_single python scripts/one_torus.py > gpurun_out/ncu_torus.log 2>&1
+# the wide-band launch (MODE 2 instantiation) of the second torus field
+timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:ptp_run4_kernel<float, \(bool\)0, \(int\)2>' -s 1 -c 1 -o gpurun_out/prof_torus_single python scripts/one_torus.py > gpurun_out/ncu_torus.log 2>&1
 tail -1 gpurun_out/ncu_torus.log
 timeout 600 python scripts/perf_configs.py > gpurun_out/perf_configs.txt 2>&1; tail -3 gpurun_out/perf_configs.txt
+timeout 900 python scripts/configs_report.py gpurun_out/configs.json > gpurun_out/configs.log 2>&1; tail -3 gpurun_out/configs.log
