@@ -591,21 +591,20 @@ struct WidePre {
 };
 
 // trip 1 of a wide position (issued one position ahead by the caller)
-__device__ __forceinline__ void wide_pre_f32(int p, size_t N, const int* pv, const int* pring,
+__device__ __forceinline__ void wide_pre(int p, size_t N, const int* pv, const int* pring,
                                              WidePre& w) {
     w.vr = ldcg(pv + p);
 #pragma unroll
     for (int e = 0; e < kEllW; ++e) w.raw[e] = __ldcg(pring + ell_slot(e) * N + p);
 }
 
-template <bool LABELS>
-__device__ __forceinline__ void relax_wide_f32(const MeshDev& M, const RunArgs& A, int p, int kk,
-                                               const WidePre& w, const float* pL,
-                                               const char* pquad, const float* dp, float* dc,
-                                               const int* lp, int* lc, int fe, float eps,
-                                               int& nonconv, float& my_max, long long& calls,
-                                               long long& degs) {
-    const float inf = Lim<float>::inf();
+template <typename T, bool LABELS>
+__device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, int p, int kk,
+                                            const WidePre& w, const T* pL, const char* pquad,
+                                            const T* dp, T* dc, const int* lp, int* lc, int fe,
+                                            T eps, int& nonconv, T& my_max, long long& calls,
+                                            long long& degs) {
+    const T inf = Lim<T>::inf();
     const size_t N = static_cast<size_t>(A.stride);
     const int vr = w.vr;
     int raw[kEllW];
@@ -613,41 +612,41 @@ __device__ __forceinline__ void relax_wide_f32(const MeshDev& M, const RunArgs& 
     for (int e = 0; e < kEllW; ++e) raw[e] = w.raw[e];
     const int v = vr & kIdMask;
     size_t pb = static_cast<size_t>(p), step = N;
-    const float* lsrc = pL;
+    const T* lsrc = pL;
     const char* qsrc = pquad;
     if (!(vr & kPacked)) {
         pb = static_cast<size_t>(v) * kEllW;
         step = 1;
-        lsrc = static_cast<const float*>(M.eL);
+        lsrc = static_cast<const T*>(M.eL);
         qsrc = static_cast<const char*>(M.equad);
 #pragma unroll
         for (int e = 0; e < kEllW; ++e) raw[e] = __ldcg(M.ering + pb + ell_slot(e));
     }
-    const float tv = ldcg(dp + v);
+    const T tv = ldcg(dp + v);
     const int lv = LABELS ? ldcg(lp + v) : -1;
     int d = (raw[0] >> kMetaShift) & 15;
-    float best = tv;
+    T best = tv;
     int blab = lv;
     if (d == kEllOverflow) {
         // more than 7 corners: CSR tables, sequential fan walk
         const int c0 = __ldg(M.cptr + v);
         d = __ldg(M.cptr + v + 1) - c0;
         const int r0 = c0 + v;
-        const float* ringL = static_cast<const float*>(M.ringL);
+        const T* ringL = static_cast<const T*>(M.ringL);
         int x0 = __ldg(M.ring + r0);
         int i0 = x0 & INT_MAX;
-        float t0 = ldcg(dp + i0), L0 = __ldg(ringL + r0);
+        T t0 = ldcg(dp + i0), L0 = __ldg(ringL + r0);
         int l0 = LABELS ? ldcg(lp + i0) : -1;
         for (int c = 0; c < d; ++c) {
             const int x1 = __ldg(M.ring + r0 + c + 1);
             const int i1 = x1 & INT_MAX;
-            const float t1 = ldcg(dp + i1), L1 = __ldg(ringL + r0 + c + 1);
+            const T t1 = ldcg(dp + i1), L1 = __ldg(ringL + r0 + c + 1);
             const int l1 = LABELS ? ldcg(lp + i1) : -1;
-            Quad<float> q;
+            Quad<T> q;
             q.load(M.quad, c0 + c);
             const bool mixed = LABELS && l0 != l1 && t0 != inf && t1 != inf;
             int side, deg;
-            const float val = corner_eval<float>(t0, t1, L0, L1, q, x0 < 0, mixed, side, deg);
+            const T val = corner_eval<T>(t0, t1, L0, L1, q, x0 < 0, mixed, side, deg);
             degs += deg;
             if (val < best) {
                 best = val;
@@ -656,22 +655,23 @@ __device__ __forceinline__ void relax_wide_f32(const MeshDev& M, const RunArgs& 
             x0 = x1; i0 = i1; t0 = t1; L0 = L1; l0 = l1;
         }
     } else if (d > 0) {
-        float t[kEllW + 1], L[kEllW];
+        // fp32: every live quad is loaded with the distances (one trip); fp64: the quads
+        // of a corner pair are loaded as the pair is reached (register budget)
+        constexpr int kQ = sizeof(T) == 4 ? kEllW : 1;
+        T t[kEllW + 1], L[kEllW];
         int l[kEllW + 1];
-        Quad<float> q[kEllW];
+        Quad<T> q[kQ];
 #pragma unroll
         for (int e = 0; e <= kEllW; ++e) {
             t[e] = inf;
             l[e] = -1;
-            if (e < kEllW) {
-                L[e] = 0.0f;
-                q[e].q11 = q[e].q12 = q[e].q22 = q[e].a = 0.0f;
-            }
+            if (e < kEllW) L[e] = T(0);
+            if (e < kQ) q[e].q11 = q[e].q12 = q[e].q22 = q[e].a = T(0);
             if (e < kEllW && e <= d) {
                 t[e] = ldcg(dp + (raw[e] & kIdMask));
                 if (LABELS) l[e] = ldcg(lp + (raw[e] & kIdMask));
                 L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
-                if (e < d) q[e].load_cg(qsrc, pb + ell_slot(e) * step);
+                if (e < kQ && e < d) q[e].load_cg(qsrc, pb + ell_slot(e) * step);
             }
         }
 #pragma unroll
@@ -679,26 +679,39 @@ __device__ __forceinline__ void relax_wide_f32(const MeshDev& M, const RunArgs& 
             if (c >= d) break;  // valence 6: three pairs, not four
             const bool m0 = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
             const bool m1 = LABELS && l[c + 1] != l[c + 2] && t[c + 1] != inf && t[c + 2] != inf;
-            float val[2];
+            T val[2];
             int side[2], deg[2];
-            const float t1v[2] = {t[c], t[c + 1]}, t2v[2] = {t[c + 1], t[c + 2]};
-            const float L1v[2] = {L[c], L[c + 1]};
-            const float L2v[2] = {L[c + 1], c + 2 < kEllW ? L[c + 2] : 0.0f};
-            const Quad<float> qv[2] = {q[c], q[c + 1]};
-            const bool dgv[2] = {raw[c] < 0, raw[c + 1] < 0};
-            const bool mix[2] = {m0, m1};
-            const bool valid[2] = {c < d, c + 1 < d};
-            corner_pair_f32(t1v, t2v, L1v, L2v, qv, dgv, mix, valid, val, side, deg);
+            if constexpr (sizeof(T) == 4) {
+                const float t1v[2] = {t[c], t[c + 1]}, t2v[2] = {t[c + 1], t[c + 2]};
+                const float L1v[2] = {L[c], L[c + 1]};
+                const float L2v[2] = {L[c + 1], c + 2 < kEllW ? L[c + 2] : 0.0f};
+                const Quad<float> qv[2] = {q[c % kQ], q[(c + 1) % kQ]};
+                const bool dgv[2] = {raw[c] < 0, raw[c + 1] < 0};
+                const bool mix[2] = {m0, m1};
+                const bool valid[2] = {c < d, c + 1 < d};
+                corner_pair_f32(t1v, t2v, L1v, L2v, qv, dgv, mix, valid, val, side, deg);
+            } else {
+                Quad<T> q0, q1;
+                q0.load_cg(qsrc, pb + ell_slot(c) * step);
+                val[0] = corner_eval<T>(t[c], t[c + 1], L[c], L[c + 1], q0, raw[c] < 0, m0,
+                                        side[0], deg[0]);
+                if (c + 1 < d) {
+                    q1.load_cg(qsrc, pb + ell_slot(c + 1) * step);
+                    val[1] = corner_eval<T>(t[c + 1], t[c + 2], L[c + 1],
+                                            L[c + 2 < kEllW ? c + 2 : c + 1], q1, raw[c + 1] < 0,
+                                            m1, side[1], deg[1]);
+                } else {
+                    val[1] = inf;
+                    deg[1] = 0;
+                    side[1] = -1;
+                }
+            }
             if (!(c + 1 < d)) {
                 val[1] = inf;
                 deg[1] = 0;
             }
-            if (!(c < d)) {
-                val[0] = inf;
-                deg[0] = 0;
-            }
             degs += deg[0] + deg[1];
-            if (c < d && val[0] < best) {
+            if (val[0] < best) {
                 best = val[0];
                 if (LABELS) blab = side[0] == 0 ? l[c] : l[c + 1];
             }
@@ -712,7 +725,7 @@ __device__ __forceinline__ void relax_wide_f32(const MeshDev& M, const RunArgs& 
     if (LABELS) lc[v] = blab;
     calls += d;
     if (p < fe || A.last_change != nullptr) {
-        const float rc = rel_change(tv, best);
+        const T rc = rel_change(tv, best);
         if (p < fe && rc >= eps) nonconv = 1;
         if (p < fe && rc > my_max) my_max = rc;
         if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
@@ -1091,7 +1104,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
             // (the wide-only instantiation has no narrow path to protect: fp64 too, but
             // not fp64 with labels, whose per-thread fan spills)
-            constexpr bool kThreadWide = sizeof(T) == 4 || (MODE == 2 && !LABELS);
+            constexpr bool kThreadWide = sizeof(T) == 4 || MODE == 2;
             // Wide iterations (fp32): positions are dealt to CTAs in chunks of 32
             // consecutive positions (chunk c -> CTA c mod nb) instead of one by one, so
             // a warp works on 32 neighbouring positions: their records are adjacent and,
@@ -1171,7 +1184,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if constexpr (kThreadWide) {
                 // older band positions [bb, oe): one vertex per thread, chunked
                 auto pos = [&](int t) { return bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk); };
-                if constexpr (kWide2 && sizeof(T) == 4) {
+                if constexpr (kWide2) {
                     // software-pipelined: trip 1 of the next position is in flight while
                     // this one's distances are gathered and its corners evaluated
                     // (not with labels: the second record in flight spills registers)
@@ -1179,26 +1192,26 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     int t = tid;
                     int p = pos(t);
                     WidePre nx;
-                    if constexpr (LABELS) {
+                    if constexpr (LABELS || sizeof(T) == 8) {
                         for (;; t += kBlock) {
                             p = pos(t);
                             if (p - (t % kChunk) >= oe_) break;
                             if (p < oe_) {
-                                wide_pre_f32(p, N, pv, pring, nx);
-                                relax_wide_f32<LABELS>(M, A, p, kk, nx, pL, pquad, dp, dcur, lp,
+                                wide_pre(p, N, pv, pring, nx);
+                                relax_wide2<T, LABELS>(M, A, p, kk, nx, pL, pquad, dp, dcur, lp,
                                                        lc, fe_, eps, nonconv, my_max, calls, degs);
                             }
                         }
                     } else {
-                    if (p - (t % kChunk) < oe_ && p < oe_) wide_pre_f32(p, N, pv, pring, nx);
+                    if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
                     while (p - (t % kChunk) < oe_) {
                         const WidePre cw = nx;
                         const int pc = p;
                         t += kBlock;
                         p = pos(t);
-                        if (p - (t % kChunk) < oe_ && p < oe_) wide_pre_f32(p, N, pv, pring, nx);
+                        if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
                         if (pc < oe_)
-                            relax_wide_f32<LABELS>(M, A, pc, kk, cw, pL, pquad, dp, dcur, lp, lc,
+                            relax_wide2<T, LABELS>(M, A, pc, kk, cw, pL, pquad, dp, dcur, lp, lc,
                                                    fe_, eps, nonconv, my_max, calls, degs);
                     }
                     }

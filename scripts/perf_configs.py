@@ -42,6 +42,15 @@ if "fps" in which:
     t = time.perf_counter()
     r = g.farthest_point_sampling(M, 16, seed=0, precision="single")
     out["torus_fps16_single_s"] = time.perf_counter() - t
+if "fps32" in which:
+    # ab.sh-friendly: {precision: {"ms": wall ms for 32 FPS rounds}}
+    M = g.generate_torus(1000, 1000)
+    out["torus_fps32"] = {}
+    for prec in ("single", "double"):
+        g.farthest_point_sampling(M, 2, seed=0, precision=prec)
+        t = time.perf_counter()
+        g.farthest_point_sampling(M, 32, seed=0, precision=prec)
+        out["torus_fps32"][prec] = {"ms": 1e3 * (time.perf_counter() - t)}
 if "batch" in which:
     M = g.generate_torus(1000, 1000)
     n = M.n_vertices
