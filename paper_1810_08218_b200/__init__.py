@@ -52,7 +52,7 @@ class Mesh:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _capi._lib is not None:
+        if h and _capi is not None and getattr(_capi, "_lib", None) is not None:
             _capi._lib.geodist_mesh_destroy(h)
             self._h = None
 

@@ -1052,9 +1052,10 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
                          void* stream) {
     if (groups <= 0 && nq >= 3 && mesh && config && sources && offsets && out_dist) {
         // Automatic grouping: query 0 runs on the whole GPU; its mean band per CTA
-        // tells whether fields here are latency-bound (narrow bands: many concurrent
-        // groups raise throughput, measured 2x at 8 groups on the icosphere-8) or
-        // throughput-bound (wide bands: one group is fastest, e.g. the 1000^2 torus).
+        // chooses the number of concurrent fields.  Narrow bands are latency-bound per
+        // iteration (16 groups: 2.1x the single-field throughput on the icosphere-8);
+        // wide ones gain less but still gain (the 1000^2 torus: 4 groups, 1.2x; the
+        // grid barrier is amortised over more work per CTA).  scripts/batch_probe.py.
         geodist_ptp_stats s0{};
         int rc = geodist_batch_device(mesh, sources, offsets, 1, config, out_dist, out_labels,
                                       &s0, 1, stream);
@@ -1063,7 +1064,9 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, M(mesh)->device);
         const double band = s0.iterations > 0 ? double(s0.vertex_updates) / s0.iterations : 0.0;
         const double per_cta = band / std::max(1, sms);
-        const int g = per_cta < 160 ? 8 : per_cta < 400 ? 4 : per_cta < 800 ? 2 : 1;
+        const int g = per_cta < 600 ? 16 : per_cta < 1200 ? 8 : 4;
+        if (std::getenv("GEODIST_DEBUG_GROUPS"))
+            std::fprintf(stderr, "batch auto-grouping: band per CTA %.0f -> %d groups\n", per_cta, g);
         std::vector<int32_t> off(nq);
         for (int q = 1; q <= nq - 1; ++q) off[q - 1] = offsets[q] - offsets[1];
         off[nq - 1] = offsets[nq] - offsets[1];

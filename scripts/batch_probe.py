@@ -7,8 +7,11 @@ import paper_1810_08218_b200 as g
 
 mesh_name = sys.argv[1] if len(sys.argv) > 1 else "torus"
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+labels = False
 if mesh_name == "torus":
     M = g.generate_torus(1000, 1000)
+elif mesh_name == "height":
+    M = g.heightfield_grid(2048, 2048)
 else:
     v, f = g.noisy_icosphere_arrays(8, 2e-3, 1)
     M = g.Mesh(v, f)
@@ -16,8 +19,8 @@ n = M.n_vertices
 qs = [[q * (n // 512)] for q in range(nq)]
 out = torch.empty((nq, n), dtype=torch.float32, device="cuda")
 res = {}
-for groups in (1, 2, 4, 8):
-    g.batch_geodesics_device(M, qs[:groups], out.data_ptr(), groups=groups)  # warm
+for groups in (1, 2, 4, 8, 16, 0):
+    g.batch_geodesics_device(M, qs[:max(groups, 3)], out.data_ptr(), groups=groups)  # warm
     torch.cuda.synchronize()
     t = time.perf_counter()
     st = g.batch_geodesics_device(M, qs, out.data_ptr(), groups=groups)
