@@ -407,182 +407,12 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
 // shuffles, no idle corner slots, record bookkeeping once per vertex): the
 // sequential strict-'<' fan scan of relax_vertex (update_kernel.hpp:93-120),
 // corners evaluated two at a time.
-template <typename T> __device__ __forceinline__ void load_L8_cg(const T* base, size_t pb, T* L);
-template <> __device__ __forceinline__ void load_L8_cg<float>(const float* base, size_t pb, float* L) {
-    const float4* q = reinterpret_cast<const float4*>(base + pb);
-    const float4 a = __ldcg(q), b = __ldcg(q + 1);
-    L[0] = a.x; L[4] = a.y; L[1] = a.z; L[5] = a.w;
-    L[2] = b.x; L[6] = b.y; L[3] = b.z; L[7] = b.w;
-}
-template <> __device__ __forceinline__ void load_L8_cg<double>(const double* base, size_t pb, double* L) {
-    const double2* q = reinterpret_cast<const double2*>(base + pb);
-    const double2 a = __ldcg(q), b = __ldcg(q + 1), c = __ldcg(q + 2), d = __ldcg(q + 3);
-    L[0] = a.x; L[4] = a.y; L[1] = b.x; L[5] = b.y;
-    L[2] = c.x; L[6] = c.y; L[3] = d.x; L[7] = d.y;
-}
-
-// The record half of a wide task, loaded one task ahead (wide_load) so that its
-// trips overlap the previous task's relaxation (relax_wide).
-template <typename T> struct WideRec {
-    int p, vr;
-    int raw[kEllW];
-    T L[kEllW];
-};
-
-template <typename T>
-__device__ __forceinline__ void wide_load(const MeshDev& M, const RunArgs& A, int p,
-                                          const int* pv, const int* pring, const T* pL,
-                                          WideRec<T>& r) {
-    r.p = p;
-    r.vr = ldcg(pv + p);
-    const int v = r.vr & kIdMask;
-    // packed records are slot-major (slot s of position p at s * N + p): a warp on 32
-    // consecutive positions reads each slot as one contiguous run
-    size_t pb = static_cast<size_t>(p), step = static_cast<size_t>(A.stride);
-    const int* rsrc = pring;
-    const T* lsrc = pL;
-    if (!(r.vr & kPacked)) {
-        // no packed record (the vertex entered the band while it was narrow): ELL by id
-        pb = static_cast<size_t>(v) * kEllW;
-        step = 1;
-        rsrc = M.ering;
-        lsrc = static_cast<const T*>(M.eL);
-    }
-#pragma unroll
-    for (int e = 0; e < kEllW; ++e) {
-        r.raw[e] = __ldcg(rsrc + pb + ell_slot(e) * step);
-        r.L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
-    }
-}
-
-template <typename T, bool LABELS>
-__device__ __forceinline__ void relax_wide(const MeshDev& M, const RunArgs& A,
-                                           const WideRec<T>& rec, int kk, const char* pquad,
-                                           const T* dp, T* dc, const int* lp, int* lc, int fe,
-                                           T eps, int& nonconv, T& my_max, long long& calls,
-                                           long long& degs) {
-    const T inf = Lim<T>::inf();
-    const int p = rec.p;
-    const int v = rec.vr & kIdMask;
-    size_t pb = static_cast<size_t>(p), step = static_cast<size_t>(A.stride);
-    const char* qsrc = pquad;
-    if (!(rec.vr & kPacked)) {
-        pb = static_cast<size_t>(v) * kEllW;
-        step = 1;
-        qsrc = static_cast<const char*>(M.equad);
-    }
-    const int* raw = rec.raw;
-    const T* L = rec.L;
-    const T tv = ldcg(dp + v);
-    const int lv = LABELS ? ldcg(lp + v) : -1;
-    int d = (raw[0] >> kMetaShift) & 15;
-    T best = tv;
-    int blab = lv;
-    if (d == kEllOverflow) {
-        // more than 7 corners: CSR tables, sequential fan walk
-        const int c0 = __ldg(M.cptr + v);
-        d = __ldg(M.cptr + v + 1) - c0;
-        const int r0 = c0 + v;
-        const T* ringL = static_cast<const T*>(M.ringL);
-        int x0 = __ldg(M.ring + r0);
-        int i0 = x0 & INT_MAX;
-        T t0 = ldcg(dp + i0), L0 = __ldg(ringL + r0);
-        int l0 = LABELS ? ldcg(lp + i0) : -1;
-        for (int c = 0; c < d; ++c) {
-            const int x1 = __ldg(M.ring + r0 + c + 1);
-            const int i1 = x1 & INT_MAX;
-            const T t1 = ldcg(dp + i1), L1 = __ldg(ringL + r0 + c + 1);
-            const int l1 = LABELS ? ldcg(lp + i1) : -1;
-            Quad<T> q;
-            q.load(M.quad, c0 + c);
-            const bool mixed = LABELS && l0 != l1 && t0 != inf && t1 != inf;
-            int side, deg;
-            const T val = corner_eval<T>(t0, t1, L0, L1, q, x0 < 0, mixed, side, deg);
-            degs += deg;
-            if (val < best) {
-                best = val;
-                if (LABELS) blab = side == 0 ? l0 : l1;
-            }
-            x0 = x1; i0 = i1; t0 = t1; L0 = L1; l0 = l1;
-        }
-    } else if (d > 0) {
-        T t[kEllW + 1];
-        int l[kEllW + 1];
-#pragma unroll
-        for (int e = 0; e <= kEllW; ++e) {
-            t[e] = inf;
-            l[e] = -1;
-            if (e < kEllW && e <= d) {
-                t[e] = ldcg(dp + (raw[e] & kIdMask));
-                if (LABELS) l[e] = ldcg(lp + (raw[e] & kIdMask));
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < kEllW - 1; c += 2) {
-            Quad<T> q0, q1;
-            q0.load_cg(qsrc, pb + ell_slot(c) * step);
-            q1.load_cg(qsrc, pb + ell_slot(c + 1) * step);
-            const bool m0 = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
-            const bool m1 = LABELS && l[c + 1] != l[c + 2] && t[c + 1] != inf && t[c + 2] != inf;
-            T val[2];
-            int side[2], deg[2];
-            if constexpr (sizeof(T) == 4) {
-                const float t1v[2] = {t[c], t[c + 1]}, t2v[2] = {t[c + 1], t[c + 2]};
-                const float L1v[2] = {L[c], L[c + 1]};
-                const float L2v[2] = {L[c + 1], c + 2 < kEllW ? L[c + 2] : 0.0f};
-                const Quad<float> qv[2] = {q0, q1};
-                const bool dgv[2] = {raw[c] < 0, raw[c + 1] < 0};
-                const bool mix[2] = {m0, m1};
-                const bool valid[2] = {c < d, c + 1 < d};
-                corner_pair_f32(t1v, t2v, L1v, L2v, qv, dgv, mix, valid, val, side, deg);
-            } else {
-                val[0] = corner_eval<T>(t[c], t[c + 1], L[c], L[c + 1], q0, raw[c] < 0, m0,
-                                        side[0], deg[0]);
-                if (c + 1 < d)
-                    val[1] = corner_eval<T>(t[c + 1], t[c + 2], L[c + 1], L[c + 2 < kEllW ? c + 2 : c + 1],
-                                            q1, raw[c + 1] < 0, m1, side[1], deg[1]);
-                else {
-                    val[1] = inf;
-                    deg[1] = 0;
-                    side[1] = -1;
-                }
-                if (!(c < d)) {
-                    val[0] = inf;
-                    deg[0] = 0;
-                }
-            }
-            degs += deg[0] + deg[1];
-            if (c < d && val[0] < best) {
-                best = val[0];
-                if (LABELS) blab = side[0] == 0 ? l[c] : l[c + 1];
-            }
-            if (c + 1 < d && val[1] < best) {
-                best = val[1];
-                if (LABELS) blab = side[1] == 0 ? l[c + 1] : l[c + 2];
-            }
-        }
-    }
-    dc[v] = best;
-    if (LABELS) lc[v] = blab;
-    calls += d;
-    if (p < fe || A.last_change != nullptr) {
-        const T rc = rel_change(tv, best);
-        if (p < fe && rc >= eps) nonconv = 1;
-        if (p < fe && rc > my_max) my_max = rc;
-        if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
-    }
-}
-
-#ifndef GEODIST_WIDE2
-#define GEODIST_WIDE2 1
-#endif
-constexpr bool kWide2 = GEODIST_WIDE2 != 0;
-
-// fp32 wide relaxation, one vertex per thread, arranged for memory-level parallelism:
+// Wide relaxation, one vertex per thread, arranged for memory-level parallelism:
 // trip 1 loads the position's vertex id AND its packed ring ids (both addressed by the
 // position: slot s of p at s * N + p), trip 2 the neighbours' distances together with
 // |x| and the corner quads of the d live slots only, then the corners are evaluated.
-// (relax_wide's order -- vertex id, then ring ids, then distances -- was three trips.)
+// (the first version's order -- vertex id, then ring ids, then distances -- was three
+// trips.)
 // A position without a packed record (entered the band while it was narrow) re-reads
 // its ring ids from the id-indexed ELL table: one more trip for those only.
 struct WidePre {
@@ -1146,7 +976,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             }
             } else {
             for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
-                // fp32: the newest topleset here, older ones in relax_wide below; fp64: all
+                // the newest topleset here, older ones one vertex per thread below (relax_wide2)
                 const int wbase = kThreadWide ? oe_ : bb_;
                 const int p = wbase + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
                 const bool act = p < be_;
@@ -1184,7 +1014,6 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if constexpr (kThreadWide) {
                 // older band positions [bb, oe): one vertex per thread, chunked
                 auto pos = [&](int t) { return bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk); };
-                if constexpr (kWide2) {
                     // software-pipelined: trip 1 of the next position is in flight while
                     // this one's distances are gathered and its corners evaluated
                     // (not with labels: the second record in flight spills registers)
@@ -1215,18 +1044,6 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                                                    fe_, eps, nonconv, my_max, calls, degs);
                     }
                     }
-                } else {
-                    for (int t = tid;; t += kBlock) {
-                        const int p = pos(t);
-                        if (p - (t % kChunk) >= oe_) break;
-                        if (p < oe_) {
-                            WideRec<T> rec;
-                            wide_load<T>(M, A, p, pv, pring, pL, rec);
-                            relax_wide<T, LABELS>(M, A, rec, kk, pquad, dp, dcur, lp, lc, fe_,
-                                                  eps, nonconv, my_max, calls, degs);
-                        }
-                    }
-                }
             }
             }
             if (dbg) dslot[7] = cyc();
