@@ -129,6 +129,20 @@ int geodist_mesh_fans(geodist_mesh_t mesh, int32_t* cptr, int32_t* ring, int32_t
 int geodist_build_fans(const double* xyz, int32_t n, const int32_t* faces, int32_t nf,
                        int32_t* cptr, int32_t* ring, int32_t* degree);
 
+/* Mesh files (load_mesh / write_mesh, mesh_io.cpp:119-156): ASCII OFF or OBJ chosen
+ * by the extension, triangles only, validated; errors are GEODIST_EMESH with the
+ * reference's message ("<path>: ...").  load parses the whole file into a handle
+ * (n vertices, nf faces), copy fills caller arrays (xyz 3n doubles, faces 3nf), free
+ * releases it.  write uses "%.17g" coordinates (reading back is bit-exact). */
+typedef struct geodist_meshfile_s* geodist_meshfile_t;
+#define GEODIST_FORMAT_OFF 0
+#define GEODIST_FORMAT_OBJ 1
+int geodist_meshfile_load(const char* path, geodist_meshfile_t* out, int32_t* n, int32_t* nf);
+int geodist_meshfile_copy(geodist_meshfile_t file, double* xyz, int32_t* faces);
+int geodist_meshfile_free(geodist_meshfile_t file);
+int geodist_write_mesh(const char* path, const double* xyz, int32_t n, const int32_t* faces,
+                       int32_t nf, int32_t format);
+
 /* validate_mesh (mesh.cpp:11-34): GEODIST_EMESH with the reference's message. */
 int geodist_validate_mesh(const double* xyz, int32_t n, const int32_t* faces, int32_t nf);
 

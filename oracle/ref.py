@@ -34,6 +34,8 @@ def lib():
         L.ref_mesh_create.argtypes = [_f64p, C.c_int, _i32p, C.c_int, C.POINTER(C.c_void_p),
                                       C.POINTER(C.c_double)]
         L.ref_mesh_destroy.argtypes = [C.c_void_p]
+        L.ref_load_mesh.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.ref_write_mesh.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
         L.ref_generate_grid.argtypes = [C.c_int, C.c_int, C.c_double, C.POINTER(C.c_void_p)]
         L.ref_generate_icosphere.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
         L.ref_mesh_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -104,6 +106,16 @@ class RefMesh:
         m = cls(h)
         m.build_seconds = secs.value
         return m
+
+    @classmethod
+    def load(cls, path):
+        """geodist::load_mesh (mesh_io.cpp): arrays() only -- no connectivity is built."""
+        h = C.c_void_p()
+        _check(lib().ref_load_mesh(str(path).encode(), C.byref(h)))
+        return cls(h)
+
+    def write(self, path, obj=False):
+        _check(lib().ref_write_mesh(self.h, str(path).encode(), int(bool(obj))))
 
     @classmethod
     def grid(cls, nx, ny, shear=0.0):

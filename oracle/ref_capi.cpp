@@ -13,6 +13,8 @@
 //   ref_voronoi     -> geodist::voronoi             (src/sampling.cpp:51-58)
 //   ref_planar      -> geodist::planar_update<T>    (include/geodist/update_kernel.hpp:34-79)
 //   ref_fan         -> Connectivity::for_each_incident_triangle (connectivity.hpp:35-44)
+//   ref_load_mesh   -> geodist::load_mesh             (src/mesh_io.cpp:119-139)
+//   ref_write_mesh  -> geodist::write_mesh            (src/mesh_io.cpp:141-156)
 //
 // Every function returns 0 on success, 1 for std::invalid_argument, 2 for
 // std::runtime_error / anything else; the message is kept in ref_last_error().
@@ -30,6 +32,7 @@
 
 #include "geodist/connectivity.hpp"
 #include "geodist/mesh.hpp"
+#include "geodist/mesh_io.hpp"
 #include "geodist/ptp.hpp"
 #include "geodist/sampling.hpp"
 #include "geodist/toplesets.hpp"
@@ -97,6 +100,27 @@ int ref_mesh_create(const double* xyz, int n, const int* faces, int nf, void** o
 }
 
 void ref_mesh_destroy(void* h) { delete static_cast<Handle*>(h); }
+
+// load_mesh into a handle WITHOUT building connectivity (the file reader alone)
+int ref_load_mesh(const char* path, void** out) {
+    return guarded([&] {
+        auto* h = new Handle;
+        try {
+            h->mesh = load_mesh(std::string(path));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int ref_write_mesh(void* hp, const char* path, int obj) {
+    return guarded([&] {
+        write_mesh(static_cast<Handle*>(hp)->mesh, std::string(path),
+                   obj ? MeshFormat::obj : MeshFormat::off);
+    });
+}
 
 static void* wrap(TriangleMesh m) {
     auto* h = new Handle;

@@ -13,6 +13,7 @@ entry points raise.
 """
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -21,7 +22,8 @@ from ._capi import check, lib, ptr
 
 __all__ = [
     "Mesh", "farthest_point_sampling", "generate_grid", "generate_icosphere", "generate_torus",
-    "geodesics", "grid_reference", "heightfield_grid", "load_mesh", "mape", "mesh_from_arrays",
+    "geodesics", "grid_reference", "heightfield_grid", "load_mesh", "read_mesh", "write_mesh",
+    "mape", "mesh_from_arrays",
     "noisy_icosphere", "sphere_reference", "toplesets", "voronoi", "reorder_for_bands",
     "batch_geodesics", "planar_update", "device_count",
 ]
@@ -191,40 +193,38 @@ def mesh_from_arrays(vertices, faces, device=0):
     return Mesh(v, f, device=device)
 
 
+def read_mesh(path):
+    """Parse an ASCII OFF / OBJ file (load_mesh, mesh_io.cpp:119-139: format from the
+    extension, triangles only, validated) into (vertices float64 (n,3), faces int32 (m,3)).
+    Host-only: the native reader in csrc/mesh_io.cpp; errors raise RuntimeError with the
+    reference's message."""
+    h = C.c_void_p()
+    n, nf = C.c_int32(), C.c_int32()
+    check(lib().geodist_meshfile_load(os.fsencode(str(path)), C.byref(h), C.byref(n), C.byref(nf)))
+    try:
+        v = np.empty(3 * n.value + 1, np.float64)
+        f = np.empty(3 * nf.value + 1, np.int32)
+        check(lib().geodist_meshfile_copy(h, v, f))
+    finally:
+        lib().geodist_meshfile_free(h)
+    return v[:3 * n.value].reshape(-1, 3), f[:3 * nf.value].reshape(-1, 3)
+
+
 def load_mesh(path, device=0):
-    """OFF / OBJ reader (mesh_io.cpp:32-115 formats; triangles only)."""
-    verts, faces = [], []
-    with open(path) as fh:
-        text = fh.read()
-    if path.lower().endswith(".off"):
-        toks = [ln.split("#")[0].split() for ln in text.splitlines()]
-        toks = [t for t in toks if t]
-        head = toks[0]
-        if head[0].upper() != "OFF":
-            raise RuntimeError(f"{path}: missing OFF header")
-        counts = head[1:] if len(head) > 1 else toks[1]
-        start = 1 if len(head) > 1 else 2
-        nv, nf = int(counts[0]), int(counts[1])
-        for t in toks[start:start + nv]:
-            verts.append([float(x) for x in t[:3]])
-        for t in toks[start + nv:start + nv + nf]:
-            if int(t[0]) != 3:
-                raise RuntimeError(f"{path}: only triangle faces are supported")
-            faces.append([int(x) for x in t[1:4]])
-    else:
-        for ln in text.splitlines():
-            t = ln.split()
-            if not t:
-                continue
-            if t[0] == "v":
-                verts.append([float(x) for x in t[1:4]])
-            elif t[0] == "f":
-                idx = [int(x.split("/")[0]) - 1 for x in t[1:]]
-                if len(idx) != 3:
-                    raise RuntimeError(f"{path}: only triangle faces are supported")
-                faces.append(idx)
-    return Mesh(np.array(verts, np.float64).reshape(-1, 3), np.array(faces, np.int32).reshape(-1, 3),
-                device=device)
+    """Mesh from an OFF / OBJ file (bindings.cpp load_mesh)."""
+    v, f = read_mesh(path)
+    return Mesh(v, f, device=device)
+
+
+def write_mesh(path, vertices, faces, fmt=None):
+    """write_mesh (mesh_io.cpp:141-156): "%.17g" coordinates, OFF or OBJ (from the
+    extension unless fmt is 'off' / 'obj')."""
+    if fmt is None:
+        fmt = "obj" if str(path).lower().endswith(".obj") else "off"
+    v = np.ascontiguousarray(vertices, np.float64).reshape(-1)
+    f = np.ascontiguousarray(faces, np.int32).reshape(-1)
+    check(lib().geodist_write_mesh(os.fsencode(str(path)), v, len(v) // 3, f, len(f) // 3,
+                                   1 if fmt == "obj" else 0))
 
 
 # ---------------------------------------------------------------------------

@@ -19,6 +19,7 @@ EXPORTED = [
     "geodist_last_error", "geodist_version", "geodist_device_count", "geodist_mesh_create",
     "geodist_mesh_destroy", "geodist_mesh_sizes", "geodist_mesh_degrees", "geodist_mesh_fan",
     "geodist_mesh_fans",
+    "geodist_meshfile_load", "geodist_meshfile_copy", "geodist_meshfile_free", "geodist_write_mesh",
     "geodist_build_fans", "geodist_validate_mesh", "geodist_build_halfedges", "geodist_grid_sizes", "geodist_generate_grid", "geodist_icosphere_sizes",
     "geodist_generate_icosphere", "geodist_perturb_radial", "geodist_torus_sizes",
     "geodist_generate_torus", "geodist_heightfield", "geodist_toplesets",
@@ -81,6 +82,12 @@ def lib():
         L.geodist_mesh_fan.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.c_int32,
                                        C.POINTER(C.c_int32)]
         L.geodist_mesh_fans.argtypes = [_vp, _i32p, _i32p, _i32p]
+        L.geodist_meshfile_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p),
+                                            C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.geodist_meshfile_copy.argtypes = [_vp, _f64p, _i32p]
+        L.geodist_meshfile_free.argtypes = [_vp]
+        L.geodist_write_mesh.argtypes = [C.c_char_p, _f64p, C.c_int32, _i32p, C.c_int32,
+                                         C.c_int32]
         L.geodist_build_fans.argtypes = [_f64p, C.c_int32, _i32p, C.c_int32, _i32p, _i32p, _vp]
         L.geodist_validate_mesh.argtypes = [_f64p, C.c_int32, _i32p, C.c_int32]
         L.geodist_build_halfedges.argtypes = [_vp, C.c_int32, _i32p, C.c_int32, _i32p, _i32p]

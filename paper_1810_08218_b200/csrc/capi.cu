@@ -732,6 +732,43 @@ int geodist_build_fans(const double* xyz, int32_t n, const int32_t* faces, int32
     });
 }
 
+struct geodist_meshfile_s {
+    MeshData m;
+};
+
+int geodist_meshfile_load(const char* path, geodist_meshfile_t* out, int32_t* n, int32_t* nf) {
+    return guarded([&] {
+        if (!path || !out) throw Fail(GEODIST_EINVAL, "null argument");
+        *out = nullptr;
+        std::unique_ptr<geodist_meshfile_s> f(new geodist_meshfile_s);
+        load_mesh_file(path, f->m);  // runtime_error -> EMESH (the reference's text)
+        if (n) *n = static_cast<int32_t>(f->m.xyz.size() / 3);
+        if (nf) *nf = static_cast<int32_t>(f->m.faces.size() / 3);
+        *out = f.release();
+    });
+}
+
+int geodist_meshfile_copy(geodist_meshfile_t file, double* xyz, int32_t* faces) {
+    return guarded([&] {
+        if (!file) throw Fail(GEODIST_EINVAL, "null mesh file handle");
+        if (xyz) std::copy(file->m.xyz.begin(), file->m.xyz.end(), xyz);
+        if (faces) std::copy(file->m.faces.begin(), file->m.faces.end(), faces);
+    });
+}
+
+int geodist_meshfile_free(geodist_meshfile_t file) {
+    return guarded([&] { delete file; });
+}
+
+int geodist_write_mesh(const char* path, const double* xyz, int32_t n, const int32_t* faces,
+                       int32_t nf, int32_t format) {
+    return guarded([&] {
+        if (!path || (n > 0 && !xyz) || (nf > 0 && !faces) || n < 0 || nf < 0)
+            throw Fail(GEODIST_EINVAL, "invalid mesh arrays");
+        write_mesh_file(path, xyz, n, faces, nf, format == GEODIST_FORMAT_OFF);
+    });
+}
+
 int geodist_validate_mesh(const double* xyz, int32_t n, const int32_t* faces, int32_t nf) {
     return guarded([&] { validate(xyz, n, faces, nf); });
 }

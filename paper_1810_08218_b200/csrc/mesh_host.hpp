@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 namespace gdb {
@@ -18,6 +19,15 @@ struct Fans {
 };
 
 void validate(const double* xyz, int32_t n, const int32_t* faces, int32_t nf);
+
+// Mesh files (mesh_io.cpp): ASCII OFF / OBJ by extension, validated.
+struct MeshData {
+    std::vector<double> xyz;      // 3 n
+    std::vector<int32_t> faces;   // 3 nf
+};
+void load_mesh_file(const std::string& path, MeshData& m);
+void write_mesh_file(const std::string& path, const double* xyz, int32_t n, const int32_t* faces,
+                     int32_t nf, bool off);
 Fans build_fans(const double* xyz, int32_t n, const int32_t* faces, int32_t nf);
 
 void generate_grid(int32_t nx, int32_t ny, double shear, double* xyz, int32_t* faces);
