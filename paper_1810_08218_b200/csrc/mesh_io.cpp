@@ -1,7 +1,7 @@
 // Mesh file ingestion: ASCII OFF and Wavefront OBJ, the formats and
 // the error behaviour of the reference's load_mesh / write_mesh (src/mesh_io.cpp:32-115,
 // 133-160), without a std::istringstream per line: the file is read in one block and
-// parsed in place, numbers with std::from_chars.
+// parsed in place by one thread per chunk of lines, numbers with std::from_chars.
 //
 // Token rules follow the reference's stream extraction (libstdc++ num_get): a number is
 // the longest run of characters its grammar accepts, and that whole run must convert
@@ -14,9 +14,11 @@
 #include <charconv>
 #include <cstdint>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mesh_host.hpp"
@@ -120,6 +122,43 @@ struct Lines {
     }
 };
 
+// The body of a file is cut into chunks at line boundaries and parsed by one thread
+// per chunk in two passes: count the records of every chunk (content lines for OFF,
+// v / f records for OBJ), then parse each chunk straight into the output arrays at its
+// prefix offsets.  A chunk stops at its first bad record; the first chunk (in file
+// order) that stopped names the error, so the message is the one the reference's
+// sequential reader gives.
+std::vector<Cursor> split_chunks(const char* b, const char* e) {
+    const size_t len = static_cast<size_t>(e - b);
+    unsigned hw = std::thread::hardware_concurrency();
+    const unsigned T = len < (4u << 20) ? 1u : std::max(1u, std::min(hw ? hw : 1u, 32u));
+    std::vector<Cursor> ch;
+    const char* x = b;
+    for (unsigned t = 0; t < T; ++t) {
+        const char* y = t + 1 == T ? e : b + len * (t + 1) / T;
+        if (y < x) y = x;
+        if (y < e) {
+            const char* nl = static_cast<const char*>(std::memchr(y, '\n', e - y));
+            y = nl ? nl + 1 : e;
+        }
+        ch.push_back({x, y});
+        x = y;
+    }
+    return ch;
+}
+
+template <typename Fn>
+void parallel_for(size_t n, Fn&& fn) {
+    if (n <= 1) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (size_t i = 0; i < n; ++i) th.emplace_back([&fn, i] { fn(i); });
+    for (auto& t : th) t.join();
+}
+
 void load_off(const std::string& path, const std::string& text, MeshData& m) {
     Lines L{text.data(), text.data() + text.size()};
     Cursor c;
@@ -138,33 +177,70 @@ void load_off(const std::string& path, const std::string& text, MeshData& m) {
                 parse_fail(path, "malformed element counts");
         }
     }
+    (void)ne;
     if (nv < 0 || nf < 0) parse_fail(path, "negative element counts");
-    m.xyz.clear();
-    m.faces.clear();
-    m.xyz.reserve(3 * static_cast<size_t>(std::min<long long>(nv, 1LL << 28)));
-    for (long long v = 0; v < nv; ++v) {
-        if (!L.next_content(c)) parse_fail(path, "unexpected end of file in vertex " + std::to_string(v));
-        double x, y, z;
-        if (!(read_double(c, x) && read_double(c, y) && read_double(c, z)))
-            parse_fail(path, "malformed vertex " + std::to_string(v));
-        m.xyz.push_back(x);
-        m.xyz.push_back(y);
-        m.xyz.push_back(z);
+    const std::vector<Cursor> ch = split_chunks(L.p, L.end);
+    const size_t C = ch.size();
+    // pass 1: content lines per chunk
+    std::vector<long long> cnt(C + 1, 0);
+    parallel_for(C, [&](size_t k) {
+        Lines l{ch[k].p, ch[k].e};
+        Cursor x;
+        long long n = 0;
+        while (l.next_content(x)) ++n;
+        cnt[k + 1] = n;
+    });
+    for (size_t k = 0; k < C; ++k) cnt[k + 1] += cnt[k];
+    const long long total = cnt[C];
+    const long long nv_have = std::min(total, nv);
+    const long long nf_have = std::max(0LL, std::min(total - nv, nf));
+    m.xyz.assign(3 * static_cast<size_t>(nv_have), 0.0);
+    m.faces.assign(3 * static_cast<size_t>(nf_have), 0);
+    // pass 2: parse; err_at = global content-line index of the chunk's first bad line
+    std::vector<long long> err_at(C, -1), err_k(C, 0);
+    parallel_for(C, [&](size_t k) {
+        Lines l{ch[k].p, ch[k].e};
+        Cursor x;
+        for (long long g = cnt[k]; g < nv + nf && l.next_content(x); ++g) {
+            if (g < nv) {
+                double a, b, d;
+                if (!(read_double(x, a) && read_double(x, b) && read_double(x, d))) {
+                    err_at[k] = g;
+                    return;
+                }
+                double* o = &m.xyz[3 * static_cast<size_t>(g)];
+                o[0] = a; o[1] = b; o[2] = d;
+            } else {
+                long long kk, a, b, d;
+                if (!read_ll(x, kk)) {
+                    err_at[k] = g;
+                    err_k[k] = LLONG_MIN;
+                    return;
+                }
+                if (kk != 3 || !(read_ll(x, a) && read_ll(x, b) && read_ll(x, d))) {
+                    err_at[k] = g;
+                    err_k[k] = kk;
+                    return;
+                }
+                int32_t* o = &m.faces[3 * static_cast<size_t>(g - nv)];
+                o[0] = static_cast<int32_t>(a);
+                o[1] = static_cast<int32_t>(b);
+                o[2] = static_cast<int32_t>(d);
+            }
+        }
+    });
+    for (size_t k = 0; k < C; ++k) {
+        const long long g = err_at[k];
+        if (g < 0) continue;
+        if (g < nv) parse_fail(path, "malformed vertex " + std::to_string(g));
+        const long long f = g - nv;
+        if (err_k[k] == LLONG_MIN || err_k[k] == 3) parse_fail(path, "malformed face " + std::to_string(f));
+        parse_fail(path, "face " + std::to_string(f) + " has " + std::to_string(err_k[k]) +
+                             " vertices, only triangles are supported");
     }
-    m.faces.reserve(3 * static_cast<size_t>(std::min<long long>(nf, 1LL << 28)));
-    for (long long f = 0; f < nf; ++f) {
-        if (!L.next_content(c)) parse_fail(path, "unexpected end of file in face " + std::to_string(f));
-        long long k, a, b, d;
-        if (!read_ll(c, k)) parse_fail(path, "malformed face " + std::to_string(f));
-        if (k != 3)
-            parse_fail(path, "face " + std::to_string(f) + " has " + std::to_string(k) +
-                                 " vertices, only triangles are supported");
-        if (!(read_ll(c, a) && read_ll(c, b) && read_ll(c, d)))
-            parse_fail(path, "malformed face " + std::to_string(f));
-        m.faces.push_back(static_cast<int32_t>(a));
-        m.faces.push_back(static_cast<int32_t>(b));
-        m.faces.push_back(static_cast<int32_t>(d));
-    }
+    if (total < nv) parse_fail(path, "unexpected end of file in vertex " + std::to_string(total));
+    if (total < nv + nf)
+        parse_fail(path, "unexpected end of file in face " + std::to_string(total - nv));
 }
 
 int32_t obj_corner_index(const char* t0, const char* t1, size_t nv, const std::string& path,
@@ -181,44 +257,78 @@ int32_t obj_corner_index(const char* t0, const char* t1, size_t nv, const std::s
     return static_cast<int32_t>(idx - 1);
 }
 
+// 'v' / 'f' / other for the line's first token
+inline int obj_tag(Cursor& x) {
+    const char *t0, *t1;
+    if (!read_token(x, t0, t1) || t1 - t0 != 1) return 0;
+    return *t0 == 'v' ? 1 : *t0 == 'f' ? 2 : 0;
+}
+
 void load_obj(const std::string& path, const std::string& text, MeshData& m) {
-    Lines L{text.data(), text.data() + text.size()};
-    Cursor c;
-    long long f_records = 0;
-    m.xyz.clear();
-    m.faces.clear();
-    while (L.next(c)) {
-        const char *t0, *t1;
-        if (!read_token(c, t0, t1)) continue;
-        const size_t tl = static_cast<size_t>(t1 - t0);
-        if (tl == 1 && *t0 == 'v') {
-            double x, y, z;
-            if (!(read_double(c, x) && read_double(c, y) && read_double(c, z)))
-                parse_fail(path, "malformed v record " + std::to_string(m.xyz.size() / 3));
-            m.xyz.push_back(x);
-            m.xyz.push_back(y);
-            m.xyz.push_back(z);
-        } else if (tl == 1 && *t0 == 'f') {
-            const char* tok[3][2];
-            int cnt = 0;
-            const char *a0, *a1;
-            while (read_token(c, a0, a1)) {
-                if (cnt < 3) {
-                    tok[cnt][0] = a0;
-                    tok[cnt][1] = a1;
-                }
-                ++cnt;
-            }
-            if (cnt != 3)
-                parse_fail(path, "f record " + std::to_string(f_records) + " has " +
-                                     std::to_string(cnt) + " corners, only triangles are supported");
-            const size_t nv = m.xyz.size() / 3;
-            for (int k = 0; k < 3; ++k)
-                m.faces.push_back(obj_corner_index(tok[k][0], tok[k][1], nv, path, f_records));
-            ++f_records;
+    const std::vector<Cursor> ch = split_chunks(text.data(), text.data() + text.size());
+    const size_t C = ch.size();
+    std::vector<long long> nvk(C + 1, 0), nfk(C + 1, 0);
+    parallel_for(C, [&](size_t k) {
+        Lines l{ch[k].p, ch[k].e};
+        Cursor x;
+        long long a = 0, b = 0;
+        while (l.next(x)) {
+            const int t = obj_tag(x);
+            a += t == 1;
+            b += t == 2;
         }
-        // vt / vn / usemtl / ... records are ignored
+        nvk[k + 1] = a;
+        nfk[k + 1] = b;
+    });
+    for (size_t k = 0; k < C; ++k) {
+        nvk[k + 1] += nvk[k];
+        nfk[k + 1] += nfk[k];
     }
+    m.xyz.assign(3 * static_cast<size_t>(nvk[C]), 0.0);
+    m.faces.assign(3 * static_cast<size_t>(nfk[C]), 0);
+    std::vector<std::string> err(C);
+    parallel_for(C, [&](size_t k) {
+        Lines l{ch[k].p, ch[k].e};
+        Cursor x;
+        long long v = nvk[k], f = nfk[k];
+        try {
+            while (l.next(x)) {
+                const int t = obj_tag(x);
+                if (t == 1) {
+                    double a, b, d;
+                    if (!(read_double(x, a) && read_double(x, b) && read_double(x, d)))
+                        parse_fail(path, "malformed v record " + std::to_string(v));
+                    double* o = &m.xyz[3 * static_cast<size_t>(v)];
+                    o[0] = a; o[1] = b; o[2] = d;
+                    ++v;
+                } else if (t == 2) {
+                    const char* tok[3][2];
+                    int cnt = 0;
+                    const char *a0, *a1;
+                    while (read_token(x, a0, a1)) {
+                        if (cnt < 3) {
+                            tok[cnt][0] = a0;
+                            tok[cnt][1] = a1;
+                        }
+                        ++cnt;
+                    }
+                    if (cnt != 3)
+                        parse_fail(path, "f record " + std::to_string(f) + " has " +
+                                             std::to_string(cnt) +
+                                             " corners, only triangles are supported");
+                    int32_t* o = &m.faces[3 * static_cast<size_t>(f)];
+                    for (int q = 0; q < 3; ++q)
+                        o[q] = obj_corner_index(tok[q][0], tok[q][1], static_cast<size_t>(v), path, f);
+                    ++f;
+                }
+                // vt / vn / usemtl / ... records are ignored
+            }
+        } catch (const std::runtime_error& e) {
+            err[k] = e.what();
+        }
+    });
+    for (size_t k = 0; k < C; ++k)
+        if (!err[k].empty()) throw std::runtime_error(err[k]);
 }
 
 }  // namespace

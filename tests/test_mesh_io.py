@@ -127,3 +127,39 @@ def test_reader_errors_without_reference(tmp_path):
         g.read_mesh(p)
     with pytest.raises(RuntimeError, match="unsupported mesh format"):
         g.read_mesh(tmp_path / "x.stl")
+
+
+@needs_ref
+@pytest.mark.parametrize("ext", ["off", "obj"])
+def test_chunked_parse_matches_reference(tmp_path, ext):
+    """Files above the chunking threshold (4 MiB): relative OBJ indices resolved across
+    chunk boundaries, and the first error in file order wins over later ones."""
+    v, f = g.grid_arrays(400, 400, 0.25)  # 10-20 MB: several chunks
+    p = tmp_path / f"big.{ext}"
+    g.write_mesh(p, v, f)
+    if ext == "obj":
+        # rewrite every face with relative (negative) indices interleaved after its vertices
+        lines = [f"v {float(x[0])!r} {float(x[1])!r} {float(x[2])!r}" for x in v]
+        out = []
+        k = 0
+        for t, tri in enumerate(f):
+            need = int(max(tri)) + 1
+            while k < need:
+                out.append(lines[k])
+                k += 1
+            out.append("f " + " ".join(str(int(i) - k) for i in tri))
+        out += lines[k:]
+        p.write_text("\n".join(out) + "\n")
+    a, b = both(p)
+    assert not isinstance(a, str) and not isinstance(b, str)
+    assert np.array_equal(a[0].view(np.int64), b[0].view(np.int64)) and np.array_equal(a[1], b[1])
+    text = p.read_text().splitlines()
+    n = len(text)
+    for early, late in ((n // 5, 4 * n // 5), (4 * n // 5, n - 2)):
+        bad = list(text)
+        for at in (early, late):
+            bad[at] = "v 1 x 2" if ext == "obj" else ("1 x 2" if at < 1 + len(v) + 1 else "4 1 2 3 4")
+        q = tmp_path / f"bad.{ext}"
+        q.write_text("\n".join(bad) + "\n")
+        a, b = both(q)
+        assert isinstance(b, str) and a == b
