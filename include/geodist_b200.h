@@ -232,6 +232,11 @@ int geodist_planar_update(const double* x1, const double* x2, const double* t1, 
                           int32_t count, int32_t precision, double* value, int32_t* side,
                           int32_t* degenerate);
 
+/* Self-test of the kernels' straight-line div/sqrt fast paths against the IEEE
+ * intrinsics over n pseudo-random operand pairs: counts[0..7] = (accepted, differing)
+ * for fp64 div, fp64 sqrt, fp32 div, fp32 sqrt.  "differing" must be 0. */
+int geodist_selftest_arith(int64_t n, uint64_t seed, int64_t* counts);
+
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t geodist_kernel_launches(void);
 

@@ -25,7 +25,7 @@ EXPORTED = [
     "geodist_generate_torus", "geodist_heightfield", "geodist_toplesets",
     "geodist_reorder_for_bands", "geodist_ptp", "geodist_ptp_ordered", "geodist_voronoi",
     "geodist_fps", "geodist_batch_device", "geodist_batch", "geodist_planar_update",
-    "geodist_kernel_launches",
+    "geodist_kernel_launches", "geodist_selftest_arith",
 ]
 
 
@@ -82,6 +82,8 @@ def lib():
         L.geodist_mesh_fan.argtypes = [_vp, C.c_int32, _i32p, _i32p, C.c_int32,
                                        C.POINTER(C.c_int32)]
         L.geodist_mesh_fans.argtypes = [_vp, _i32p, _i32p, _i32p]
+        L.geodist_selftest_arith.argtypes = [C.c_int64, C.c_uint64,
+                                             np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
         L.geodist_meshfile_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p),
                                             C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.geodist_meshfile_copy.argtypes = [_vp, _f64p, _i32p]

@@ -1293,6 +1293,19 @@ int geodist_batch(geodist_mesh_t mesh, const int32_t* sources, const int32_t* of
     });
 }
 
+int geodist_selftest_arith(int64_t n, uint64_t seed, int64_t* counts) {
+    return guarded([&] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        require_device(dev);
+        std::unique_ptr<void, DFree> out(dalloc<unsigned long long>(8));
+        cuda_ok(cudaMemset(out.get(), 0, 64), "memset");
+        launch_arith_selftest(n, seed, static_cast<unsigned long long*>(out.get()), nullptr);
+        cuda_ok(cudaGetLastError(), "arith_selftest_kernel");
+        cuda_ok(cudaMemcpy(counts, out.get(), 64, cudaMemcpyDeviceToHost), "d2h");
+    });
+}
+
 int geodist_planar_update(const double* x1, const double* x2, const double* t1, const double* t2,
                           int32_t count, int32_t precision, double* value, int32_t* side,
                           int32_t* degenerate) {

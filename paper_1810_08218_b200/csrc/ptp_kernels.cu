@@ -1464,6 +1464,67 @@ void launch_planar_test(int precision, const double* x1, const double* x2, const
     note_launch();
 }
 
+// Self-test of the straight-line div/sqrt fast paths (ptp_common.cuh) against the
+// IEEE intrinsics on pseudo-random operands spanning the exponent range: counts the
+// operands each fast path accepts (checked) and those where it differs (mismatch).
+// out[0..7] = fp64 div checked, mismatch, fp64 sqrt checked, mismatch, fp32 div ...,
+// fp32 sqrt ...
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+    return x ^ (x >> 33);
+}
+__global__ void arith_selftest_kernel(long long n, unsigned long long seed,
+                                      unsigned long long* out) {
+    unsigned long long c[8] = {};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long h1 = mix64(seed ^ (2 * i)), h2 = mix64(seed ^ (2 * i + 1));
+        // doubles: random mantissa and sign, exponent in [-300, 300] (and a few edges)
+        auto mk = [](unsigned long long h) {
+            const unsigned long long e = 1023 - 300 + (h >> 52) % 601;
+            return __longlong_as_double(static_cast<long long>(((h & 1ull) << 63) | (e << 52) |
+                                                               (h >> 12 & 0xfffffffffffffull)));
+        };
+        const double x = mk(h1), y = mk(h2);
+        bool ok;
+        const double q = div_with_recip64(x, y, div_recip64(y), ok);
+        if (ok) {
+            ++c[0];
+            c[1] += __double_as_longlong(q) != __double_as_longlong(__ddiv_rn(x, y));
+        }
+        const double ax = fabs(x);
+        const double r = sqrt_fast64(ax, ok);
+        if (ok) {
+            ++c[2];
+            c[3] += __double_as_longlong(r) != __double_as_longlong(__dsqrt_rn(ax));
+        }
+        // floats: exponent in [-80, 80]
+        auto mkf = [](unsigned long long h) {
+            const unsigned e = 127 - 80 + static_cast<unsigned>((h >> 40) % 161);
+            return __uint_as_float(static_cast<unsigned>((h & 1ull) << 31) | (e << 23) |
+                                   static_cast<unsigned>(h >> 9 & 0x7fffffu));
+        };
+        const float xf = mkf(h1), yf = mkf(h2);
+        if (div_operand_ok(xf) && div_operand_ok(yf)) {
+            ++c[4];
+            const float qf = div_with_recip(xf, yf, div_recip(yf));
+            c[5] += __float_as_uint(qf) != __float_as_uint(__fdiv_rn(xf, yf));
+        }
+        const float af = fabsf(xf);
+        if (sqrt_fast_ok(af)) {
+            ++c[6];
+            c[7] += __float_as_uint(sqrt_fast(af)) != __float_as_uint(__fsqrt_rn(af));
+        }
+    }
+    for (int k = 0; k < 8; ++k) atomicAdd(out + k, c[k]);
+}
+
+void launch_arith_selftest(long long n, unsigned long long seed, unsigned long long* out,
+                           cudaStream_t st) {
+    arith_selftest_kernel<<<4 * 148, 256, 0, st>>>(n, seed, out);
+    note_launch();
+}
+
 __global__ void reset_bars_kernel(GroupCtl* ctl, int groups) {
     for (int g = threadIdx.x; g < groups; g += blockDim.x) {
         ctl[g].bar = 0u;

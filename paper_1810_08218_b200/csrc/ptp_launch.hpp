@@ -18,6 +18,9 @@ void launch_planar_test(int precision, const double* x1, const double* x2, const
                         const double* t2, int count, double* value, int* side, int* degen,
                         cudaStream_t st);
 
+void launch_arith_selftest(long long n, unsigned long long seed, unsigned long long* out,
+                           cudaStream_t st);
+
 // Max co-resident CTAs of the run kernel on `device` (cooperative launch bound).
 // version 3: claimer-first solver (default); version 2: general queue-based solver
 // (used when a CTA's claims overflow its shared-memory list).

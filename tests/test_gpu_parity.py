@@ -249,3 +249,15 @@ def test_reference_properties():
     S = g.generate_icosphere(3)
     rep = g.mape(g.geodesics(S, [0])["distances"], g.sphere_reference(S, [0]), [0])
     assert rep["mape"] < 3.0
+
+
+def test_fast_path_arithmetic_is_ieee():
+    """The straight-line div.rn / sqrt.rn sequences the kernels use (fp32 and fp64,
+    ptp_common.cuh) return the IEEE correctly rounded result on every operand they
+    accept: 2^26 pseudo-random pairs over a wide exponent range."""
+    from paper_1810_08218_b200 import _capi
+    counts = np.zeros(8, np.int64)
+    g.check(_capi.lib().geodist_selftest_arith(1 << 26, 12345, counts))
+    acc, bad = counts[0::2], counts[1::2]
+    assert (acc > (1 << 24)).all(), counts
+    assert (bad == 0).all(), counts
