@@ -131,11 +131,20 @@ def config_block(n, precision, nranks):
             "parallelism": f"independent fields, {nranks} rank(s)"}
 
 
+def host_threads():
+    """All host threads this process may run on.  (torchrun exports OMP_NUM_THREADS=1, so
+    the reference's 'workers = 0 -> omp_get_max_threads()' would run it on one thread.)"""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_reference_field(V, F, precision, src=0):
     """One field on the unmodified reference (oracle/_ref), all host threads."""
     from oracle import ref
     R = ref.RefMesh.from_arrays(V, F)
-    r = R.ptp([src], precision=precision, workers=0)
+    r = R.ptp([src], precision=precision, workers=host_threads())
     return R, r
 
 
@@ -151,11 +160,11 @@ def run_reference(args):
     R = ref.RefMesh.from_arrays(V, F)
     times = []
     for s in range(args.warmup + args.steps):
-        r = R.ptp([source_for(0, s, len(V))], precision=args.precision, workers=0)
+        r = R.ptp([source_for(0, s, len(V))], precision=args.precision, workers=host_threads())
         if s >= args.warmup:
             times.append(r["wall_seconds"] + r["toplesets_seconds"])
     ms = 1e3 * sum(times) / len(times)
-    cores = ref.max_threads()
+    cores = int(r["workers"])
     line = {"metric": "ms per distance field @1M verts", "value": ms, "unit": "ms",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
@@ -313,7 +322,7 @@ def main():
                     same = np.array_equal(mine.view(np.int64), r["distances"].view(np.int64))
                     line["cpu_baseline"] = {
                         "value": 1e3 * (r["wall_seconds"] + r["toplesets_seconds"]), "unit": "ms",
-                        "cores": ref.max_threads(), "kind": "reference",
+                        "cores": int(r["workers"]), "kind": "reference",
                         "sample": "1 field, source 0 (compute_toplesets + ptp_run, reference "
                                   "timers), unmodified reference built by oracle/Makefile",
                         "ptp_run_ms": 1e3 * r["wall_seconds"],
