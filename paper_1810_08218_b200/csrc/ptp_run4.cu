@@ -523,11 +523,11 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
             } else {
                 Quad<T> q0, q1;
                 q0.load_cg(qsrc, pb + ell_slot(c) * step);
-                val[0] = corner_eval<T>(t[c], t[c + 1], L[c], L[c + 1], q0, raw[c] < 0, m0,
+                val[0] = corner_eval_f64<true>(t[c], t[c + 1], L[c], L[c + 1], q0, raw[c] < 0, m0,
                                         side[0], deg[0]);
                 if (c + 1 < d) {
                     q1.load_cg(qsrc, pb + ell_slot(c + 1) * step);
-                    val[1] = corner_eval<T>(t[c + 1], t[c + 2], L[c + 1],
+                    val[1] = corner_eval_f64<true>(t[c + 1], t[c + 2], L[c + 1],
                                             L[c + 2 < kEllW ? c + 2 : c + 1], q1, raw[c + 1] < 0,
                                             m1, side[1], deg[1]);
                 } else {
