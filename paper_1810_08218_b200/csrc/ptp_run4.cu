@@ -146,20 +146,9 @@ struct ClaimCtx {
     int* err;
 };
 
-// A task whose record and distances were staged in shared memory by the
-// wide-band pipeline (pipeline_wide).
-template <typename T> struct StageIn {
-    int2 rr;
-    T La, Lb;
-    Quad<T> qa, qb;
-    int v;
-    T ta, tb, tv;
-    int la, lb, lv;
-};
-
 // Relax the vertex at BFS position p (4-lane group; relax_vertex,
 // update_kernel.hpp:93-120).  Lanes return their claims in (ca, ia, cb, ib).
-template <typename T, bool LABELS, bool STAGED = false>
+template <typename T, bool LABELS>
 __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
                                        int sl, bool act, bool is_new, bool cached, bool pack,
                                        int p, int kk, const int* pv, const int* pring, const T* pL,
@@ -169,7 +158,6 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                                        long long& calls, long long& degs, bool& ca_claim,
                                        int& ida, bool& cb_claim, int& idb,
                                        unsigned long long* tdbg,
-                                       const StageIn<T>& sin = StageIn<T>{},
                                        unsigned long long* kdbg = nullptr,
                                        unsigned long long it0 = 0) {
     const T inf = Lim<T>::inf();
@@ -186,15 +174,7 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     qb = qa;
     const int ci = sl * 4 + gl;
     bool hit = false;
-    if (STAGED) {
-        hit = true;
-        v = sin.v;
-        rr = sin.rr;
-        La = sin.La;
-        Lb = sin.Lb;
-        qa = sin.qa;
-        qb = sin.qb;
-    } else if (act && cached && !is_new) {
+    if (act && cached && !is_new) {
         const int2 tg = C.pv[ci];
         if (tg.x == p) {
             hit = true;
@@ -281,32 +261,17 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     int lv = -1;
     T ta = inf, tb = inf;
     int la = -1, lb_ = -1;
-    if (STAGED) {
-        if (act && gl == 0) {
-            tv = sin.tv;
-            lv = sin.lv;
-        }
-        if (hasa) {
-            ta = sin.ta;
-            la = sin.la;
-        }
-        if (hasb) {
-            tb = sin.tb;
-            lb_ = sin.lb;
-        }
-    } else {
-        if (act && gl == 0) {
-            tv = ldcg(dp + v);
-            if (LABELS) lv = ldcg(lp + v);
-        }
-        if (hasa) {
-            ta = ldcg(dp + ida);
-            if (LABELS) la = ldcg(lp + ida);
-        }
-        if (hasb) {
-            tb = ldcg(dp + idb);
-            if (LABELS) lb_ = ldcg(lp + idb);
-        }
+    if (act && gl == 0) {
+        tv = ldcg(dp + v);
+        if (LABELS) lv = ldcg(lp + v);
+    }
+    if (hasa) {
+        ta = ldcg(dp + ida);
+        if (LABELS) la = ldcg(lp + ida);
+    }
+    if (hasb) {
+        tb = ldcg(dp + idb);
+        if (LABELS) lb_ = ldcg(lp + idb);
     }
     // BFS claims (toplesets.cpp:44-52), issued after the distance loads: an atomic
     // ahead of them in the memory pipeline would delay the loads
@@ -959,7 +924,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
                                   cached, pack, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
                                   expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
-                                  cb, ib, (dbg && t == 0) ? dslot : nullptr, StageIn<T>{},
+                                  cb, ib, (dbg && t == 0) ? dslot : nullptr,
                                   kd, it0);
                 if (expand)
                     claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
@@ -992,7 +957,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
                                   cached, pack, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
                                   expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
-                                  cb, ib, (dbg && t == 0) ? dslot : nullptr, StageIn<T>{},
+                                  cb, ib, (dbg && t == 0) ? dslot : nullptr,
                                   kd, it0);
                 if (expand)
                     claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
