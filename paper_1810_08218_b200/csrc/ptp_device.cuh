@@ -24,6 +24,13 @@
 namespace gdb {
 
 constexpr int kBlock = 512;        // threads per CTA
+#ifndef GEODIST_WIDE_BLOCK
+#define GEODIST_WIDE_BLOCK 512
+#endif
+// threads per CTA of the wide-only v4 instantiation (a build knob: 640 / 768 threads
+// cap registers at 96 / 80 and the spills cost 8 % / 24 % on the torus, measured)
+constexpr int kWideBlock = GEODIST_WIDE_BLOCK;
+__host__ __device__ constexpr int run4_block(int mode) { return mode == 2 ? kWideBlock : kBlock; }
 constexpr int kW = 8;              // lanes per vertex in the BFS-only kernel
 constexpr int kGroup = 4;          // lanes per vertex in the solver: 2 ring entries per lane
 constexpr int kEllW = 8;           // ELL slot: 8 ring entries (<= 7 corners) per vertex

@@ -1576,7 +1576,8 @@ cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStre
     const void* f = run_kernel_ptr(version, precision, labels);
     const size_t dyn = run_dyn_smem(version, precision, labels);
     if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    e = cudaLaunchCooperativeKernel(f, dim3(grid), dim3(kBlock), params, dyn, st);
+    e = cudaLaunchCooperativeKernel(f, dim3(grid), dim3(version >= 4 ? run4_block(version - 4) : kBlock),
+                                    params, dyn, st);
     note_launch();
     return e;
 }

@@ -534,15 +534,16 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
 // exits (state saved in GroupCtl, mode_exit = the other mode) when the band
 // crosses over, so each instantiation carries only its own path's registers.
 template <typename T, bool LABELS, int MODE>
-__global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
+__global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A) {
+    constexpr int kB = run4_block(MODE);
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ Bcast4 S;
     __shared__ int s_lim[kLimRing];
     __shared__ int s_list[kSmemClaims];
-    __shared__ T red_t[kBlock / 32];
-    __shared__ long long red_l[kBlock / 32];
-    __shared__ double red_v[kBlock / 32];
-    __shared__ int red_i[kBlock / 32];
+    __shared__ T red_t[kB / 32];
+    __shared__ long long red_l[kB / 32];
+    __shared__ double red_v[kB / 32];
+    __shared__ int red_i[kB / 32];
     __shared__ int s_ccnt, s_err;
     __shared__ unsigned long long s_bw;
 
@@ -572,8 +573,8 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
     const int n = M.n;
     const T inf = Lim<T>::inf();
     const T eps = static_cast<T>(A.eps);
-    const int gthreads = nb * kBlock;
-    const int gtid = lb * kBlock + tid;
+    const int gthreads = nb * kB;
+    const int gtid = lb * kB + tid;
     unsigned long long* barw = ctl->barw;
     int* g_list = A.blists + static_cast<size_t>(blockIdx.x) * A.claim_cap;
     const ClaimCtx CC{s_list, g_list, A.claim_cap, &s_ccnt, &s_err};
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
     };
 
     // reset the record cache tags (smem does not survive launches)
-    for (int x = tid; x < 4 * R; x += kBlock) C.pv[x] = make_int2(-1, 0);
+    for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
 
     for (int q = g; q < A.nq; q += A.groups) {
         const int s0 = A.src_off ? A.src_off[q] : 0;
@@ -695,7 +696,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
 
         if (tid == 0) s_err = 0;
         if (q != g)
-            for (int x = tid; x < 4 * R; x += kBlock) C.pv[x] = make_int2(-1, 0);
+            for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
         if (A.phase_init) {
             // reset (ptp.cpp:61-68)
             for (int v = gtid; v < n; v += gthreads) {
@@ -757,7 +758,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if (A.fused_bfs) {
                 // iteration 0: claim topleset 1 from the sources (ring walk only)
                 const int gl = tid & (kGroup - 1);
-                for (int t = lb + nb * (tid / kGroup);; t += nb * (kBlock / kGroup)) {
+                for (int t = lb + nb * (tid / kGroup);; t += nb * (kB / kGroup)) {
                     const bool act = t < m;
                     if (!__any_sync(kFull, act)) break;
                     int v = 0, c0 = 0, d = 0;
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                 });
             } else {
                 if (A.given_rho + 1 <= kLimRing) {
-                    for (int r = tid; r <= A.given_rho; r += kBlock) s_lim[r] = ldcg(limits + r);
+                    for (int r = tid; r <= A.given_rho; r += kB) s_lim[r] = ldcg(limits + r);
                 }
                 __syncthreads();
                 if (tid == 0) {
@@ -835,7 +836,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if (__ldcg(&ctl->done)) return;
             const int top = ctl->bfs_open ? ctl->k + 2 : ctl->rho;
             const int lo = top - kLimRing + 1 > 0 ? top - kLimRing + 1 : 0;
-            for (int r = lo + tid; r <= top; r += kBlock) s_lim[r % kLimRing] = ldcg(limits + r);
+            for (int r = lo + tid; r <= top; r += kB) s_lim[r % kLimRing] = ldcg(limits + r);
             __syncthreads();
             if (tid == 0) {
                 k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
@@ -893,7 +894,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             const int f0 = S.f0, fa0 = S.fa0, nfz = S.nfz;
             int nonconv = 0;
             T my_max = T(0);
-            constexpr int kGroups = kBlock / kGroup;
+            constexpr int kGroups = kB / kGroup;
             // wide iterations (band beyond the record cache, fp32): the generic loop takes
             // only the newest topleset; older positions are relaxed one per thread below
             // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
@@ -987,7 +988,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     int p = pos(t);
                     WidePre nx;
                     if constexpr (LABELS || sizeof(T) == 8) {
-                        for (;; t += kBlock) {
+                        for (;; t += kB) {
                             p = pos(t);
                             if (p - (t % kChunk) >= oe_) break;
                             if (p < oe_) {
@@ -1001,7 +1002,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
                     while (p - (t % kChunk) < oe_) {
                         const WidePre cw = nx;
                         const int pc = p;
-                        t += kBlock;
+                        t += kB;
                         p = pos(t);
                         if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
                         if (pc < oe_)
@@ -1133,7 +1134,7 @@ __global__ void __launch_bounds__(kBlock, 1) ptp_run4_kernel(RunArgs A) {
             if ((tid & 31) == 0) { red_v[tid >> 5] = vmax; red_i[tid >> 5] = vidx; }
             __syncthreads();
             if (tid == 0) {
-                for (int w = 1; w < kBlock / 32; ++w)
+                for (int w = 1; w < kB / 32; ++w)
                     if (red_v[w] > vmax || (red_v[w] == vmax && red_i[w] < vidx)) {
                         vmax = red_v[w];
                         vidx = red_i[w];
