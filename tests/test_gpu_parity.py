@@ -156,6 +156,8 @@ SYNTH = [
     ("torus64x48", lambda: g.torus_arrays(64, 48), [[0], [17, 1500, 3000]]),
     ("height96", lambda: g.heightfield_arrays(96, 96, 20.0, 9.7, 13.1), [[0], [100, 5000, 9000]]),
     ("grid40_shear2", lambda: g.grid_arrays(40, 40, 2.0), [[820], [0, 1599]]),
+    # more toplesets than the on-chip limits ring holds (rho ~ 2600 > 1024 levels)
+    ("strip2600x3", lambda: g.grid_arrays(2600, 3, 0.0), [[0], [1300, 7799]]),
 ]
 
 
