@@ -263,3 +263,28 @@ def test_fast_path_arithmetic_is_ieee():
     acc, bad = counts[0::2], counts[1::2]
     assert (acc > (1 << 24)).all(), counts
     assert (bad == 0).all(), counts
+
+
+def test_degenerate_source_sets(port_lib):
+    """Every vertex a source (one topleset, no iteration), and a source on an isolated
+    vertex next to a component it cannot reach."""
+    v, f = g.icosphere_arrays(2)
+    M = g.Mesh(v, f)
+    P = port_lib.PortMesh(v, f)
+    allv = list(range(len(v)))
+    for prec in ("single", "double"):
+        got = g.geodesics(M, allv, precision=prec, labels=True)
+        want = P.ptp(allv, precision=prec, labels=True)
+        assert np.array_equal(bits(got["distances"]), bits(want["distances"]))
+        assert np.array_equal(got["labels"], want["labels"])
+        assert got["iterations"] == want["iterations"]
+    v2 = np.vstack([v, [[3.0, 3.0, 3.0]]])
+    M2 = g.Mesh(v2, f)
+    P2 = port_lib.PortMesh(v2, f)
+    for src in ([len(v)], [0, len(v)]):
+        for prec in ("single", "double"):
+            got = g.geodesics(M2, src, precision=prec, labels=True)
+            want = P2.ptp(src, precision=prec, labels=True)
+            assert np.array_equal(bits(got["distances"]), bits(want["distances"]))
+            assert np.array_equal(got["labels"], want["labels"])
+            assert got["unreached"] == want["unreached"]
