@@ -380,6 +380,11 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
 // trips.)
 // A position without a packed record (entered the band while it was narrow) re-reads
 // its ring ids from the id-indexed ELL table: one more trip for those only.
+#ifndef GEODIST_DYN_CHUNKS
+#define GEODIST_DYN_CHUNKS 1
+#endif
+constexpr bool kDynChunks = GEODIST_DYN_CHUNKS != 0;
+
 struct WidePre {
     int vr;
     int raw[kEllW];
@@ -545,6 +550,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
     __shared__ double red_v[kB / 32];
     __shared__ int red_i[kB / 32];
     __shared__ int s_ccnt, s_err;
+    __shared__ int s_chunk;  // next older-band chunk of this CTA (wide iterations)
     __shared__ unsigned long long s_bw;
 
     const int tid = threadIdx.x;
@@ -668,6 +674,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         auto publish = [&] {
             S.done = done;
             s_ccnt = 0;
+            s_chunk = 0;
             if (done) return;
             const int kk = k + 1;
             const int j = bfs_open ? kk : min(kk, rho - 1);
@@ -978,17 +985,32 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 dslot[18] = wchunk ? 1 : 0;
             }
             if constexpr (kThreadWide) {
-                // older band positions [bb, oe): one vertex per thread, chunked
+                // older band positions [bb, oe): one vertex per thread, chunked.  Warps
+                // take this CTA's chunks from a shared counter, so the warps that held the
+                // newest topleset's tasks (BFS claims: the longest chain) take fewer.
+                // Chunk m of this CTA starts at position bb + (lb + m * nb) * 32; task t
+                // below is chunk * 32 + lane.
+                const int lane = tid & 31;
+                auto grab = [&]() {
+                    int m = 0;
+                    if (kDynChunks) {
+                        if (lane == 0) m = atomicAdd(&s_chunk, 1);
+                        m = __shfl_sync(kFull, m, 0);
+                    }
+                    return m;
+                };
                 auto pos = [&](int t) { return bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk); };
+                // next task of this thread: the static deal (t + blockDim) or a fresh chunk
+                auto next_t = [&](int t) { return kDynChunks ? grab() * kChunk + lane : t + kB; };
                     // software-pipelined: trip 1 of the next position is in flight while
                     // this one's distances are gathered and its corners evaluated
                     // (not with labels: the second record in flight spills registers)
                     const size_t N = static_cast<size_t>(A.stride);
-                    int t = tid;
+                    int t = kDynChunks ? grab() * kChunk + lane : tid;
                     int p = pos(t);
                     WidePre nx;
                     if constexpr (LABELS || sizeof(T) == 8) {
-                        for (;; t += kB) {
+                        for (;; t = next_t(t)) {
                             p = pos(t);
                             if (p - (t % kChunk) >= oe_) break;
                             if (p < oe_) {
@@ -1002,7 +1024,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     while (p - (t % kChunk) < oe_) {
                         const WidePre cw = nx;
                         const int pc = p;
-                        t += kB;
+                        t = next_t(t);
                         p = pos(t);
                         if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
                         if (pc < oe_)
