@@ -470,8 +470,9 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
             if (e < kEllW && e <= d) {
                 t[e] = ldcg(dp + (raw[e] & kIdMask));
                 if (LABELS) l[e] = ldcg(lp + (raw[e] & kIdMask));
-                L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
-                if (e < kQ && e < d) q[e].load_cg(qsrc, pb + ell_slot(e) * step);
+                // fp64: |x| and the quads are loaded per corner pair below (registers)
+                if (sizeof(T) == 4) L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
+                if (sizeof(T) == 4 && e < kQ && e < d) q[e].load_cg(qsrc, pb + ell_slot(e) * step);
             }
         }
 #pragma unroll
@@ -493,13 +494,15 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
             } else {
                 Quad<T> q0, q1;
                 q0.load_cg(qsrc, pb + ell_slot(c) * step);
-                val[0] = corner_eval_f64<true>(t[c], t[c + 1], L[c], L[c + 1], q0, raw[c] < 0, m0,
-                                        side[0], deg[0]);
+                const T L0 = ldcg(lsrc + pb + ell_slot(c) * step);
+                const T L1 = ldcg(lsrc + pb + ell_slot(c + 1) * step);
+                val[0] = corner_eval_f64<true>(t[c], t[c + 1], L0, L1, q0, raw[c] < 0, m0,
+                                               side[0], deg[0]);
                 if (c + 1 < d) {
                     q1.load_cg(qsrc, pb + ell_slot(c + 1) * step);
-                    val[1] = corner_eval_f64<true>(t[c + 1], t[c + 2], L[c + 1],
-                                            L[c + 2 < kEllW ? c + 2 : c + 1], q1, raw[c + 1] < 0,
-                                            m1, side[1], deg[1]);
+                    const T L2 = ldcg(lsrc + pb + ell_slot(c + 2 < kEllW ? c + 2 : c + 1) * step);
+                    val[1] = corner_eval_f64<true>(t[c + 1], t[c + 2], L1, L2, q1,
+                                                   raw[c + 1] < 0, m1, side[1], deg[1]);
                 } else {
                     val[1] = inf;
                     deg[1] = 0;
