@@ -674,6 +674,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             sh_nfz = owned_count(sh_f0, frze);
         };
         int pf = -1;
+        int be_pub = 0;  // the band end publish() wrote to S.be (thread 0's copy)
+        const bool tr0 = A.trace != nullptr && lb == 0;
         auto publish = [&] {
             S.done = done;
             s_ccnt = 0;
@@ -688,6 +690,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             S.fe = fe;
             const int be = (bfs_open || j + 1 == rho) ? tail : lim(j + 1);
             S.be = be;
+            be_pub = be;
             S.oe = bfs_open ? limk : be;  // newest topleset: records still in global memory
             S.expand = bfs_open;
             S.frzb = frzb;
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             pf = -1;
             if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
                 pf = (bfs_open && i + 2 == kk + 1) ? tail : lim(i + 2);
-            if (A.trace != nullptr && lb == 0) ctl->slot[(kk + 1) % 3] = 0ull;
+            if (tr0) ctl->slot[(kk + 1) % 3] = 0ull;
             S.p0 = sh_p0;
             S.a0 = sh_a0;
             S.f0 = sh_f0;
@@ -1056,9 +1059,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 const int nnc = static_cast<int>((x >> 16) & 0xffffull);
                 const int tot = static_cast<int>(x >> 32);
                 const bool conv = nnc == 0;  // ptp.cpp:114
-                const int ub = bb, ue = S.be;
+                const int ub = bb, ue = be_pub;
                 upd += static_cast<unsigned long long>(ue - ub);
-                if (lb == 0 && A.trace != nullptr) {
+                if (tr0) {
                     const int row = kk - A.trace_k0;
                     if (row >= 0 && row < A.trace_cap) {
                         TraceRow r;
