@@ -61,6 +61,9 @@ for prec in ("double", "single"):
     cr, cms = cpu_field(R, [0], prec)
     c1[prec] = {"gpu_ms": 1e3 * gr["device_seconds"], "cpu_ms": cms, "K_gpu": gr["iterations"],
                 "K_cpu": cr["iterations"], "bit_exact": bits_equal(gr["distances"], cr["distances"])}
+diag = float(np.linalg.norm(v.max(0) - v.min(0)))
+c1["fp32_vs_fp64_max_abs_err_over_diag"] = float(
+    np.max(np.abs(gpu_field(M, [0], "single")["distances"] - R.ptp([0], precision="double")["distances"])) / diag)
 out["1_icosphere3"] = c1
 
 # 2 -------------------------------------------------------------------------------
@@ -74,6 +77,11 @@ for prec in ("single", "double"):
     c2[prec] = {"gpu_ms": 1e3 * gr["device_seconds"], "cpu_ms": cms, "K_gpu": gr["iterations"],
                 "K_cpu": cr["iterations"], "bit_exact": bits_equal(gr["distances"], cr["distances"]),
                 "U": gr["vertex_updates"], "C": gr["relax_calls"]}
+diag = float(np.linalg.norm(v.max(0) - v.min(0)))
+g32 = gpu_field(M, [0], "single", reps=1)["distances"]
+g64 = gpu_field(M, [0], "double", reps=1)["distances"]  # bit-exact with the reference's fp64
+fin = np.isfinite(g64)
+c2["fp32_vs_fp64_max_abs_err_over_diag"] = float(np.max(np.abs(g32[fin] - g64[fin])) / diag)
 out["2_noisy_icosphere8"] = c2
 del M, R
 
@@ -103,6 +111,10 @@ v, f = g.torus_arrays(1000, 1000)
 M = g.Mesh(v, f)
 R = ref.RefMesh.from_arrays(v, f)
 c4 = {}
+diag = float(np.linalg.norm(v.max(0) - v.min(0)))
+g32 = gpu_field(M, [0], "single", reps=1)["distances"]
+g64 = gpu_field(M, [0], "double", reps=1)["distances"]
+c4["single_field_fp32_vs_fp64_max_abs_err_over_diag"] = float(np.max(np.abs(g32 - g64)) / diag)
 for prec in ("double", "single"):
     g.farthest_point_sampling(M, 4, seed=0, precision=prec)  # warm
     torch.cuda.synchronize()
