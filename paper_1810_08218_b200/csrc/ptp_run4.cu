@@ -7,21 +7,24 @@
 // (corner_candidate / chunk_candidates), so results are bit-identical.  What
 // changes is where every dependent memory trip of an iteration goes:
 //
-//  * BFS position p of a query is owned by CTA p % nb for the whole solve.  A
-//    vertex's packed record (id, ELL ring, |x|, Gram quads -- the
-//    reorder_for_bands layout, toplesets.cpp:60-89) is written once at its
-//    position by the CTA that claims it, read from L2 by the owner at the
-//    vertex's first relaxation and kept in the owner's shared memory for every
-//    later iteration (a ring of R slots, slot p / nb).  An old band vertex
+//  * BFS position p of a query is owned by CTA p % nb for the whole solve.  The
+//    owner reads a vertex's record (ELL ring ids, |x|, Gram quads) once, at the
+//    vertex's first relaxation, from the id-indexed ELL tables the claimer pulled
+//    into L2 (prefetch.global.L2 at the claim), and keeps it in shared memory for
+//    every later iteration (a ring of R slots, slot p / nb).  An old band vertex
 //    therefore costs one L2 trip per iteration: the neighbour distances.
-//  * claims get their BFS position immediately (warp-aggregated atomicAdd on
-//    the queue tail) and the claimer copies the claimed vertex's ELL row into
-//    the packed record at that position while the candidates are computed.
-//  * the grid barrier is one red.release.add of a 64-bit word per CTA whose
-//    fields carry the iteration's payload: bits 0-15 arrivals, 16-31 CTAs with
-//    a front change >= eps (ptp.cpp:107,114), 32-63 claims (the next
-//    topleset's size).  Polling that word is the only trip after the barrier:
-//    topleset limits live in a shared-memory ring, not in global memory.
+//  * claims go to a per-CTA list; their BFS positions are assigned by the grid
+//    barrier itself: the arrival is one atom.acq_rel.add of a 64-bit word whose
+//    fields carry the iteration's payload (bits 0-15 arrivals, 16-31 CTAs with a
+//    front change >= eps, ptp.cpp:107,114, 32-63 claims = the next topleset's
+//    size); the value it returns is the CTA's offset in the new topleset, and
+//    warp 0 writes the list to pv[] while the CTA waits.  Topleset limits live in
+//    a shared-memory ring, so polling that word is the only trip after the barrier.
+//  * wide iterations (band beyond the record cache; MODE 2 when launched narrow /
+//    wide separately) deal positions in chunks of 32 and relax one vertex per
+//    thread from records packed by position (slot-major, reorder_for_bands layout,
+//    toplesets.cpp:60-89), written by the owner at the first relaxation once the
+//    band approaches the cache's capacity.
 #include "ptp_common.cuh"
 #include "ptp_launch.hpp"
 
