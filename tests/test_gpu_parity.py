@@ -288,3 +288,22 @@ def test_degenerate_source_sets(port_lib):
             assert np.array_equal(bits(got["distances"]), bits(want["distances"]))
             assert np.array_equal(got["labels"], want["labels"])
             assert got["unreached"] == want["unreached"]
+
+
+def test_narrow_wide_handover_parity():
+    """A field whose band grows past the record cache and shrinks back (600^2 torus: the
+    band exceeds 511 x 148 positions in iterations 239-613 of 706, so the narrow-only
+    launch hands over to the wide-only launch and back), against the unmodified
+    reference, both precisions; K and relax counts too."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("reference library not built")
+    v, f = g.torus_arrays(600, 600)
+    M = g.Mesh(v, f)
+    R = ref.RefMesh.from_arrays(v, f)
+    for prec in ("single", "double"):
+        got = g.geodesics(M, [0], precision=prec)
+        want = R.ptp([0], precision=prec, workers=0)
+        assert np.array_equal(bits(got["distances"]), bits(want["distances"])), prec
+        assert got["iterations"] == want["iterations"]
+        assert got["relax_calls"] == want["relax_calls"]
