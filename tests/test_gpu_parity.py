@@ -307,3 +307,19 @@ def test_narrow_wide_handover_parity():
         assert np.array_equal(bits(got["distances"]), bits(want["distances"])), prec
         assert got["iterations"] == want["iterations"]
         assert got["relax_calls"] == want["relax_calls"]
+
+
+def test_fps_across_handover_parity():
+    """FPS rounds (the fixed per-round launch sequence) on the 600^2 torus: the first
+    rounds' samples, labels and covering radius equal the reference's (fp64)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("reference library not built")
+    v, f = g.torus_arrays(600, 600)
+    M = g.Mesh(v, f)
+    R = ref.RefMesh.from_arrays(v, f)
+    got = g.farthest_point_sampling(M, 3, seed=0)
+    want = R.fps(3, seed=0, precision="double", workers=0)
+    assert list(got["samples"]) == list(want["samples"])
+    assert np.array_equal(got["labels"], want["labels"])
+    assert got["radius"] == want["radius"]
