@@ -192,6 +192,22 @@ def test_batch_equals_single_runs():
                 assert out["stats"][q]["relax_calls"] == one["relax_calls"]
 
 
+def test_batch_wide_bands_equal_single_runs():
+    """Batched fields whose bands exceed the record cache (600^2 torus): one group (the
+    per-query narrow/wide launch sequence), several groups (the combined kernel on 37-74
+    CTAs per field) and the automatic choice all equal the single-field path."""
+    v, f = g.torus_arrays(600, 600)
+    M = g.Mesh(v, f)
+    n = len(v)
+    queries = [[0], [n // 3], [2 * n // 3 + 17]]
+    single = [g.geodesics(M, q, precision="single") for q in queries]
+    for groups in (0, 1, 2, 4):
+        out = g.batch_geodesics(M, queries, precision="single", groups=groups)
+        for q in range(len(queries)):
+            assert np.array_equal(bits(out["distances"][q]), bits(single[q]["distances"])), groups
+            assert out["stats"][q]["iterations"] == single[q]["iterations"]
+
+
 def test_observer_monotone():
     # test_ptp.cpp:60-74: distances never increase across iterations
     M = g.generate_grid(9, 9, 2.0)
