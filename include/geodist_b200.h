@@ -2,15 +2,17 @@
  * geodist_b200.h -- C ABI of the B200-native PTP geodesic solver.
  *
  * Drop-in boundary for the reference's hot path (/root/reference/proj).  Each
- * entry point replaces one reference interface; the C++ shim
- * (include/geodist_b200/geodist.hpp) and the Python package
- * (paper_1810_08218_b200) sit on top of these calls:
+ * entry point replaces one reference interface; the C++ drop-in
+ * (integration/cpp/geodist_b200_dropin.cpp, compiled against the reference's own
+ * headers) and the Python package (paper_1810_08218_b200) sit on top of these calls:
  *
  *   geodist_mesh_create    TriangleMesh + build_connectivity, once per mesh
  *                          (include/geodist/mesh.hpp:12-23, connectivity.hpp:69,
  *                          python/bindings.cpp:26-31 MeshHandle) -> device replica
  *   geodist_toplesets      compute_toplesets (include/geodist/toplesets.hpp:32)
- *   geodist_reorder_for_bands  reorder_for_bands (toplesets.hpp:45-46)
+ *   geodist_reorder_for_bands  reorder_for_bands (toplesets.hpp:45-46) from a source set
+ *   geodist_reorder_ordered    reorder_for_bands (toplesets.hpp:45-46) from a caller's
+ *                          ToplesetOrdering (the drop-in's entry point)
  *   geodist_ptp            compute_toplesets + ptp_run (ptp.hpp:70-72) as called by
  *                          python geodesics(method="ptp") (bindings.cpp:134-151)
  *   geodist_ptp_ordered    ptp_run with a caller-supplied ToplesetOrdering (ptp.hpp:70-72)
@@ -178,6 +180,15 @@ int geodist_toplesets(geodist_mesh_t mesh, const int32_t* sources, int32_t m, in
  * old_of_new, new_of_old: n; faces_out: nf*3. */
 int geodist_reorder_for_bands(geodist_mesh_t mesh, const int32_t* sources, int32_t m,
                               int32_t* old_of_new, int32_t* new_of_old, int32_t* faces_out);
+
+/* reorder_for_bands (toplesets.cpp:60-89) for a caller-supplied ordering: sorted
+ * (reachable ids in topleset order) and position (n, -1 = unreachable), as
+ * ToplesetOrdering holds them (toplesets.hpp:16-28).  Outputs as above plus
+ * xyz_out (n*3 doubles, the permuted positions; NULL to skip; needs a mesh with
+ * positions).  A position array inconsistent with sorted is rejected. */
+int geodist_reorder_ordered(geodist_mesh_t mesh, const int32_t* sorted, int32_t reachable,
+                            const int32_t* position, int32_t* old_of_new, int32_t* new_of_old,
+                            int32_t* faces_out, double* xyz_out);
 
 /* ---- distance fields -------------------------------------------------- */
 /* compute_toplesets + ptp_run fused on the device.  distances: n doubles

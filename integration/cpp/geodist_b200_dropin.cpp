@@ -82,32 +82,46 @@ uint64_t signature(const void* data, size_t bytes, uint64_t h) {
     return h;
 }
 
+// A replica stays alive while any call uses it: the cache and every in-flight call
+// hold a reference, so an eviction (or the disabled-cache path) never destroys a
+// handle another thread is solving on.
+using ReplicaRef = std::shared_ptr<geodist_mesh_s>;
+
+ReplicaRef adopt(geodist_mesh_t h) {
+    return ReplicaRef(h, [](geodist_mesh_t p) { geodist_mesh_destroy(p); });
+}
+
 struct Replica {
     const void* vbuf;
     const void* fbuf;
     size_t nv, nf;
     uint64_t sig;
     bool geometry;
-    geodist_mesh_t h;
+    ReplicaRef h;
 };
 
 struct Cache {
     std::mutex mu;
     std::list<Replica> items;  // most recent first
-    ~Cache() {
-        for (auto& r : items) geodist_mesh_destroy(r.h);
-    }
 };
 Cache& cache() {
     static Cache c;
     return c;
 }
 
-geodist_mesh_t lookup(const void* vbuf, const void* fbuf, size_t nv, size_t nf, uint64_t sig,
-                      bool geometry, const double* xyz, const int32_t* faces) {
+ReplicaRef create(bool geometry, const double* xyz, size_t nv, const int32_t* faces, size_t nf) {
+    geodist_mesh_t h = nullptr;
+    check(geodist_mesh_create(geometry ? xyz : nullptr, static_cast<int32_t>(nv), faces,
+                              static_cast<int32_t>(nf), device_index(), &h));
+    return adopt(h);
+}
+
+ReplicaRef lookup(const void* vbuf, const void* fbuf, size_t nv, size_t nf, uint64_t sig,
+                  bool geometry, const double* xyz, const int32_t* faces) {
+    if (!cache_enabled()) return create(geometry, xyz, nv, faces, nf);  // this call's own
     Cache& c = cache();
-    std::lock_guard<std::mutex> lock(c.mu);
-    if (cache_enabled()) {
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
         for (auto it = c.items.begin(); it != c.items.end(); ++it) {
             if (it->vbuf == vbuf && it->fbuf == fbuf && it->nv == nv && it->nf == nf &&
                 it->sig == sig && (it->geometry || !geometry)) {
@@ -115,23 +129,16 @@ geodist_mesh_t lookup(const void* vbuf, const void* fbuf, size_t nv, size_t nf, 
                 return it->h;
             }
         }
-    } else {
-        for (auto& r : c.items) geodist_mesh_destroy(r.h);
-        c.items.clear();
     }
-    geodist_mesh_t h = nullptr;
-    check(geodist_mesh_create(geometry ? xyz : nullptr, static_cast<int32_t>(nv), faces,
-                              static_cast<int32_t>(nf), device_index(), &h));
+    ReplicaRef h = create(geometry, xyz, nv, faces, nf);  // built outside the lock
+    std::lock_guard<std::mutex> lock(c.mu);
     c.items.push_front({vbuf, fbuf, nv, nf, sig, geometry, h});
-    while (c.items.size() > 8) {
-        geodist_mesh_destroy(c.items.back().h);
-        c.items.pop_back();
-    }
+    while (c.items.size() > 8) c.items.pop_back();  // users keep their own reference
     return h;
 }
 
 // Replica with positions (distance fields).
-geodist_mesh_t replica(const TriangleMesh& mesh) {
+ReplicaRef replica(const TriangleMesh& mesh) {
     const size_t nv = mesh.vertices.size(), nf = mesh.faces.size();
     static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 layout");
     static_assert(sizeof(std::array<index_t, 3>) == 3 * sizeof(int32_t), "face layout");
@@ -143,7 +150,7 @@ geodist_mesh_t replica(const TriangleMesh& mesh) {
 }
 
 // Topology-only replica from a Connectivity (compute_toplesets has no mesh).
-geodist_mesh_t replica(const Connectivity& conn) {
+ReplicaRef replica(const Connectivity& conn) {
     const size_t nhe = static_cast<size_t>(conn.halfedge_count());
     std::vector<int32_t> faces(nhe);
     for (size_t h = 0; h < nhe; ++h) faces[h] = conn.origin(static_cast<index_t>(h));
@@ -276,8 +283,8 @@ ToplesetOrdering compute_toplesets(const Connectivity& conn, std::span<const ind
     out.position.resize(static_cast<size_t>(n));
     int32_t rho = 0, unreached = 0;
     if (sources.empty()) throw std::invalid_argument("compute_toplesets: empty source set");
-    geodist_mesh_t h = replica(conn);
-    check(geodist_toplesets(h, sources.data(), static_cast<int32_t>(sources.size()),
+    ReplicaRef h = replica(conn);
+    check(geodist_toplesets(h.get(), sources.data(), static_cast<int32_t>(sources.size()),
                             out.sorted.data(), out.limits.data(), out.position.data(), &rho,
                             &unreached));
     out.sorted.resize(static_cast<size_t>(n - unreached));
@@ -290,19 +297,22 @@ BandReordered reorder_for_bands(const TriangleMesh& mesh, const Connectivity& co
                                 const ToplesetOrdering& ordering) {
     (void)conn;
     const index_t n = mesh.vertex_count();
+    if (static_cast<index_t>(ordering.position.size()) != n)
+        throw std::invalid_argument("reorder_for_bands: ordering built for a different mesh");
     BandReordered out;
-    // old_of_new: the topleset order, then unreachable vertices in id order
-    out.old_of_new = ordering.sorted;
-    out.old_of_new.reserve(static_cast<size_t>(n));
-    for (index_t v = 0; v < n; ++v)
-        if (ordering.position[v] == invalid_index) out.old_of_new.push_back(v);
-    out.new_of_old.assign(static_cast<size_t>(n), invalid_index);
-    for (index_t p = 0; p < n; ++p) out.new_of_old[out.old_of_new[p]] = p;
+    // GPU: old_of_new (the topleset order, then unreachable vertices in id order),
+    // its inverse, the relabelled faces and the permuted positions (toplesets.cpp:60-89)
+    out.old_of_new.resize(static_cast<size_t>(n));
+    out.new_of_old.resize(static_cast<size_t>(n));
     out.mesh.vertices.resize(static_cast<size_t>(n));
-    for (index_t p = 0; p < n; ++p) out.mesh.vertices[p] = mesh.vertices[out.old_of_new[p]];
-    out.mesh.faces = mesh.faces;
-    for (auto& f : out.mesh.faces)
-        for (auto& x : f) x = out.new_of_old[x];
+    out.mesh.faces.resize(mesh.faces.size());
+    ReplicaRef h = replica(mesh);
+    check(geodist_reorder_ordered(h.get(), ordering.sorted.data(),
+                                  static_cast<int32_t>(ordering.sorted.size()),
+                                  ordering.position.data(), out.old_of_new.data(),
+                                  out.new_of_old.data(),
+                                  reinterpret_cast<int32_t*>(out.mesh.faces.data()),
+                                  reinterpret_cast<double*>(out.mesh.vertices.data())));
     out.conn = build_connectivity(out.mesh);
     out.ordering.limits = ordering.limits;
     out.ordering.unreached = ordering.unreached;
@@ -366,7 +376,7 @@ PtpResult ptp_run(const TriangleMesh& mesh, const Connectivity& conn,
     if (mesh.vertices.size() != ordering.position.size())
         throw std::invalid_argument("ptp_run: ordering built for a different mesh");
     const index_t n = mesh.vertex_count();
-    geodist_mesh_t h = replica(mesh);
+    ReplicaRef h = replica(mesh);
     const geodist_ptp_config cfg = make_cfg(config);
     PtpResult res;
     res.distances.values.resize(static_cast<size_t>(n));
@@ -379,7 +389,7 @@ PtpResult ptp_run(const TriangleMesh& mesh, const Connectivity& conn,
     geodist_ptp_stats st{};
     const int32_t rho = ordering.rho();
     check(geodist_ptp_ordered(
-        h, sources.data(), static_cast<int32_t>(sources.size()), ordering.sorted.data(),
+        h.get(), sources.data(), static_cast<int32_t>(sources.size()), ordering.sorted.data(),
         static_cast<int32_t>(ordering.sorted.size()), ordering.limits.data(), rho < 0 ? 0 : rho,
         ordering.position.data(), &cfg, res.distances.values.data(),
         config.with_labels ? res.distances.labels.data() : nullptr, &st,
@@ -420,14 +430,14 @@ SamplingResult fps(const TriangleMesh& mesh, const Connectivity& conn, index_t m
     if (m < 1 || m > n)
         throw std::invalid_argument("fps: sample count must be in [1, " + std::to_string(n) + "]");
     if (seed < 0 || seed >= n) throw std::invalid_argument("fps: seed vertex out of range");
-    geodist_mesh_t h = replica(mesh);
+    ReplicaRef h = replica(mesh);
     geodist_ptp_config cfg = make_cfg(config);
     cfg.with_labels = 1;
     SamplingResult out;
     out.samples.resize(static_cast<size_t>(m));
     out.labels.resize(static_cast<size_t>(n));
     std::vector<geodist_fps_row> hist(static_cast<size_t>(m));
-    check(geodist_fps(h, m, seed, &cfg, out.samples.data(), out.labels.data(), &out.radius,
+    check(geodist_fps(h.get(), m, seed, &cfg, out.samples.data(), out.labels.data(), &out.radius,
                       hist.data()));
     for (const auto& r : hist)
         out.history.push_back({r.sources, r.rho, r.relax_calls, r.radius, r.picked});
@@ -438,11 +448,11 @@ std::vector<index_t> voronoi(const TriangleMesh& mesh, const Connectivity& conn,
                              std::span<const index_t> samples, const PtpConfig& config) {
     (void)conn;
     if (samples.empty()) throw std::invalid_argument("voronoi: empty sample set");
-    geodist_mesh_t h = replica(mesh);
+    ReplicaRef h = replica(mesh);
     geodist_ptp_config cfg = make_cfg(config);
     cfg.with_labels = 1;
     std::vector<index_t> labels(static_cast<size_t>(mesh.vertex_count()));
-    check(geodist_voronoi(h, samples.data(), static_cast<int32_t>(samples.size()), &cfg,
+    check(geodist_voronoi(h.get(), samples.data(), static_cast<int32_t>(samples.size()), &cfg,
                           labels.data()));
     return labels;
 }

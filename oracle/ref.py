@@ -38,6 +38,10 @@ def lib():
         L.ref_write_mesh.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
         L.ref_generate_grid.argtypes = [C.c_int, C.c_int, C.c_double, C.POINTER(C.c_void_p)]
         L.ref_generate_icosphere.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.ref_generate_torus.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double,
+                                         C.POINTER(C.c_void_p)]
+        L.ref_perturb_radial.argtypes = [C.c_void_p, C.c_double, C.c_uint]
+        L.ref_heightfield.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
         L.ref_mesh_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_mesh_copy.argtypes = [C.c_void_p, _f64p, _i32p]
         L.ref_fan.argtypes = [C.c_void_p, C.c_int, _i32p, _i32p, C.c_int, C.POINTER(C.c_int)]
@@ -128,6 +132,27 @@ class RefMesh:
         h = C.c_void_p()
         _check(lib().ref_generate_icosphere(subdiv, C.byref(h)))
         return cls(h)
+
+    @classmethod
+    def torus(cls, nu, nv, R=3.0, r=1.0):
+        """SURVEY §8d configs 4/5 torus, generated on the reference's own types (ref_capi.cpp)."""
+        h = C.c_void_p()
+        _check(lib().ref_generate_torus(nu, nv, float(R), float(r), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def noisy_icosphere(cls, subdiv, sigma, seed=1):
+        """generate_icosphere, then p *= 1 + sigma*N(0,1), mt19937(seed)."""
+        m = cls.icosphere(subdiv)
+        lib().ref_perturb_radial(m.h, float(sigma), int(seed))
+        return m
+
+    @classmethod
+    def heightfield(cls, nx, ny, amp=20.0, wx=97.0, wy=131.0):
+        """generate_grid(nx, ny), z = amp sin(x/wx) cos(y/wy)."""
+        m = cls.grid(nx, ny, 0.0)
+        lib().ref_heightfield(m.h, float(amp), float(wx), float(wy))
+        return m
 
     def arrays(self):
         v = np.empty(self.n * 3, np.float64)

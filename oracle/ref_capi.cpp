@@ -20,8 +20,10 @@
 // std::runtime_error / anything else; the message is kept in ref_last_error().
 
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -135,6 +137,55 @@ int ref_generate_grid(int nx, int ny, double shear, void** out) {
 
 int ref_generate_icosphere(int subdiv, void** out) {
     return guarded([&] { *out = wrap(generate_icosphere(subdiv)); });
+}
+
+// SURVEY §8d synthetic inputs the reference does not ship a generator for (it has
+// generate_grid / generate_icosphere only, mesh.cpp:36-105).  Written here on the
+// reference's own types so the bench's reference arm never loads the product
+// library; tests/test_capi_host.py checks they equal the product generators.
+//   torus nu x nv, R, r: vertex (i, j) at ((R + r cos w) cos u, (R + r cos w) sin u, r sin w),
+//   u = 2 pi i / nu, w = 2 pi j / nv; quad (a, b, c, d) split (a, b, c), (a, c, d).
+int ref_generate_torus(int nu, int nv, double R, double r, void** out) {
+    return guarded([&] {
+        if (nu < 3 || nv < 3) throw std::invalid_argument("generate_torus: nu and nv must be >= 3");
+        TriangleMesh m;
+        const double two_pi = 2.0 * 3.14159265358979323846;
+        m.vertices.reserve(static_cast<size_t>(nu) * nv);
+        for (int j = 0; j < nv; ++j)
+            for (int i = 0; i < nu; ++i) {
+                const double u = two_pi * i / nu, w = two_pi * j / nv;
+                m.vertices.push_back({(R + r * std::cos(w)) * std::cos(u),
+                                      (R + r * std::cos(w)) * std::sin(u), r * std::sin(w)});
+            }
+        m.faces.reserve(2 * static_cast<size_t>(nu) * nv);
+        for (int j = 0; j < nv; ++j)
+            for (int i = 0; i < nu; ++i) {
+                const int i1 = (i + 1) % nu, j1 = (j + 1) % nv;
+                const int a = j * nu + i, b = j * nu + i1, c = j1 * nu + i1, d = j1 * nu + i;
+                m.faces.push_back({a, b, c});
+                m.faces.push_back({a, c, d});
+            }
+        *out = wrap(std::move(m));
+    });
+}
+
+// p *= 1 + sigma * N(0, 1) per vertex in index order, std::mt19937(seed) (config 2)
+void ref_perturb_radial(void* hp, double sigma, unsigned seed) {
+    auto* h = static_cast<Handle*>(hp);
+    std::mt19937 gen(seed);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    for (auto& p : h->mesh.vertices) {
+        const double f = 1.0 + sigma * normal(gen);
+        p.x *= f;
+        p.y *= f;
+        p.z *= f;
+    }
+}
+
+// z = amp * sin(x / wx) * cos(y / wy) (config 3, over generate_grid)
+void ref_heightfield(void* hp, double amp, double wx, double wy) {
+    auto* h = static_cast<Handle*>(hp);
+    for (auto& p : h->mesh.vertices) p.z = amp * std::sin(p.x / wx) * std::cos(p.y / wy);
 }
 
 void ref_mesh_sizes(void* hp, int* n, int* nf) {

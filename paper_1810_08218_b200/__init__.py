@@ -238,7 +238,12 @@ def _config(epsilon, precision, workers, labels, trace=False):
 
 
 def _sources(sources):
-    return np.ascontiguousarray(np.asarray(sources, dtype=np.int64).reshape(-1).astype(np.int32))
+    s = np.asarray(sources, dtype=np.int64).reshape(-1)
+    # index_t is int32 (vec3.hpp:8): a wider value must not wrap onto another vertex
+    bad = s[(s < np.iinfo(np.int32).min) | (s > np.iinfo(np.int32).max)]
+    if bad.size:
+        raise ValueError(f"compute_toplesets: source index {int(bad[0])} out of range")
+    return np.ascontiguousarray(s.astype(np.int32))
 
 
 def geodesics(mesh, sources, method="ptp", epsilon=1e-3, precision="double", workers=0,
@@ -333,16 +338,29 @@ def toplesets(mesh, sources):
             "unreached": unr.value, "position": pos}
 
 
-def reorder_for_bands(mesh, sources):
-    """reorder_for_bands (toplesets.cpp:60-89): returns (permuted Mesh, old_of_new, new_of_old)."""
-    src = _sources(sources)
+def reorder_for_bands(mesh, sources=None, ordering=None):
+    """reorder_for_bands (toplesets.cpp:60-89): returns (permuted Mesh, old_of_new, new_of_old).
+
+    From a source set (toplesets computed on the device), or from a caller's
+    ``ordering`` dict with ``sorted`` and ``position`` (the reference signature's
+    ToplesetOrdering, toplesets.hpp:45-46); positions are permuted on the device."""
     n, nf = mesh.n_vertices, mesh.n_faces
     oon = np.empty(n, np.int32)
     noo = np.empty(n, np.int32)
     faces = np.empty(max(3 * nf, 1), np.int32)
-    check(lib().geodist_reorder_for_bands(mesh.handle, src, len(src), ptr(oon), ptr(noo),
-                                          ptr(faces)))
-    verts = mesh._v[oon]
+    if ordering is not None:
+        srt = np.ascontiguousarray(ordering["sorted"], np.int32)
+        pos = np.ascontiguousarray(ordering["position"], np.int32)
+        if pos.shape != (n,):
+            raise ValueError("reorder_for_bands: ordering built for a different mesh")
+        verts = np.empty((n, 3), np.float64)
+        check(lib().geodist_reorder_ordered(mesh.handle, srt, len(srt), pos, ptr(oon), ptr(noo),
+                                            ptr(faces), ptr(verts)))
+    else:
+        src = _sources(sources)
+        check(lib().geodist_reorder_for_bands(mesh.handle, src, len(src), ptr(oon), ptr(noo),
+                                              ptr(faces)))
+        verts = mesh._v[oon]
     return Mesh(verts, faces[:3 * nf].reshape(-1, 3), device=mesh.device), oon, noo
 
 

@@ -23,7 +23,8 @@ EXPORTED = [
     "geodist_build_fans", "geodist_validate_mesh", "geodist_build_halfedges", "geodist_grid_sizes", "geodist_generate_grid", "geodist_icosphere_sizes",
     "geodist_generate_icosphere", "geodist_perturb_radial", "geodist_torus_sizes",
     "geodist_generate_torus", "geodist_heightfield", "geodist_toplesets",
-    "geodist_reorder_for_bands", "geodist_ptp", "geodist_ptp_ordered", "geodist_voronoi",
+    "geodist_reorder_for_bands", "geodist_reorder_ordered", "geodist_ptp", "geodist_ptp_ordered",
+    "geodist_voronoi",
     "geodist_fps", "geodist_batch_device", "geodist_batch", "geodist_planar_update",
     "geodist_kernel_launches", "geodist_selftest_arith",
 ]
@@ -108,6 +109,7 @@ def lib():
         L.geodist_toplesets.argtypes = [_vp, _i32p, C.c_int32, _vp, _vp, _vp,
                                         C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.geodist_reorder_for_bands.argtypes = [_vp, _i32p, C.c_int32, _vp, _vp, _vp]
+        L.geodist_reorder_ordered.argtypes = [_vp, _i32p, C.c_int32, _i32p, _vp, _vp, _vp, _vp]
         L.geodist_ptp.argtypes = [_vp, _i32p, C.c_int32, C.POINTER(PtpConfig), _vp, _vp,
                                   C.POINTER(PtpStats), _vp, C.c_int32, _vp, OBSERVER, _vp]
         L.geodist_ptp_ordered.argtypes = [_vp, _i32p, C.c_int32, _i32p, C.c_int32, _i32p,

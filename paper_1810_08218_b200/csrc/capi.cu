@@ -115,12 +115,12 @@ struct Workspace {
     GroupCtl* ctl = nullptr;
     unsigned long long* scratch = nullptr;  // FPS argmax, 2 words per CTA
     int scratch_blocks = 0;
-    int* pring = nullptr;                  // v3 packed records by BFS position
+    int* pring = nullptr;                  // packed records by BFS position
     void* pL = nullptr;
     void* pquad = nullptr;
-    unsigned long long* blk_slot = nullptr;  // v3 barrier payload [2][blocks] x 16 B
-    int* blists = nullptr;                 // v3 per-CTA claim lists [2][blocks][claim_cap]
+    int* blists = nullptr;                 // per-CTA claim lists [blocks][claim_cap]
     int claim_cap = 0;
+    int claim_min = 0;                     // raised after a claim-list overflow
 
     // dist0/dist1/lab0/lab1/level/queue live in one block (`hot`): the per-vertex
     // arrays every iteration gathers from.  Solver launches mark it L2-persisting so
@@ -135,9 +135,18 @@ struct Workspace {
         persisted_on = nullptr;
         for (void* p : {static_cast<void*>(limits), static_cast<void*>(ctl),
                         static_cast<void*>(scratch), static_cast<void*>(pring), pL, pquad,
-                        static_cast<void*>(blk_slot), static_cast<void*>(blists)})
+                        static_cast<void*>(blists)})
             if (p) cudaFree(p);
+        const int keep = claim_min;
         *this = Workspace();
+        claim_min = keep;
+    }
+    // A CTA claimed more vertices in one iteration than its list holds (the solve
+    // reported err 2 and stopped): the next ensure() sizes every list for the
+    // worst case (a CTA can never claim more than n vertices in one iteration).
+    void grow_claims() {
+        claim_min = static_cast<int>(std::min<long long>(n + 1, INT_MAX));
+        release();
     }
     void ensure(int g, long long nn, int blocks) {
         if (g <= groups && nn == n && blocks <= scratch_blocks) return;
@@ -166,12 +175,12 @@ struct Workspace {
         pring = dalloc<int>(e * kEllW);
         pL = dalloc<double>(e * kEllW);
         pquad = dalloc<char>(e * kEllW * 4 * sizeof(double));
-        blk_slot = dalloc<unsigned long long>(4 * static_cast<size_t>(blocks));
         // a CTA rarely claims more than a few times its share of a level; beyond the
-        // capacity the solve is redone on the general kernel (err 2)
+        // capacity the solve stops with err 2 and is redone with lists of n + 1 entries
         claim_cap = static_cast<int>(std::min<long long>(
             nn + 1, 8 * ((nn + blocks - 1) / std::max(1, blocks / std::max(1, g))) + 4096));
-        blists = dalloc<int>(2 * static_cast<size_t>(blocks) * claim_cap);
+        claim_cap = std::max(claim_cap, claim_min);
+        blists = dalloc<int>(static_cast<size_t>(blocks) * claim_cap);
     }
     // L2 access-policy window over the hot block for launches on `st`
     void persist(cudaStream_t st, int device) const {
@@ -216,7 +225,6 @@ struct Workspace {
         a.pring = pring;
         a.pL = pL;
         a.pquad = pquad;
-        a.blk_slot = blk_slot;
         a.blists = blists;
         a.claim_cap = claim_cap;
     }
@@ -386,16 +394,6 @@ void check_config(const geodist_ptp_config* c) {
         throw std::invalid_argument("precision must be 'single' or 'double'");
 }
 
-// Solver kernel: 4 = owner-cached kernel (default, ptp_run4.cu), 2 = queue-based
-// kernel, 3 = claimer-first kernel with BFS-ordered packed records
-// (GEODIST_SOLVER=2|3; 3 and 4 fall back to 2 on claim-list overflow).  Tests
-// run all of them.
-int solver_version() {
-    const char* e = getenv("GEODIST_SOLVER");
-    if (e && (e[0] == '2' || e[0] == '3')) return e[0] - '0';
-    return 4;
-}
-
 // Everything one distance-field solve needs from the caller.
 struct Solve {
     const int32_t* sources = nullptr;
@@ -417,16 +415,14 @@ struct Solve {
     int32_t rho = 0;
 };
 
-void run_solve(geodist_mesh_s* mh, const Solve& q, int version);
-
-void run_solve(geodist_mesh_s* mh, const Solve& q) { run_solve(mh, q, solver_version()); }
-
-void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
+void run_solve(geodist_mesh_s* mh, const Solve& q) {
     const int prec = q.cfg->precision;
     const bool labels = q.m > 1;  // single source: labels are provably inert
     mh->ensure_prec(prec);
     const int n = mh->n;
-    const int maxb = run_max_blocks(prec, labels, mh->device, version);
+    const int maxb = std::min(run_max_blocks(prec, labels, mh->device, 0),
+                              std::min(run_max_blocks(prec, labels, mh->device, 1),
+                                       run_max_blocks(prec, labels, mh->device, 2)));
     if (maxb <= 0) throw Fail(GEODIST_ECUDA, "run kernel cannot be resident on this device");
     mh->ws.ensure(1, n, maxb);
     Workspace& ws = mh->ws;
@@ -493,17 +489,17 @@ void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
     std::vector<double> snap;
     float total_ms = 0.f;
     GroupCtl hctl{};
-    // v4 without per-iteration host work: the narrow-band and wide-band
-    // instantiations hand the field to each other at band cross-overs (each
-    // carries only its own path's registers); otherwise the combined kernel.
-    const bool switching = version == 4 && chunk <= 0 && !getenv("GEODIST_NO_MODES");
-    int launch_version = switching ? 5 : version;
+    // Without per-iteration host work the narrow-band and wide-band instantiations
+    // hand the field to each other at band cross-overs (each carries only its own
+    // path's registers); otherwise (trace chunks, observer) the combined kernel.
+    const bool switching = chunk <= 0 && !getenv("GEODIST_NO_MODES");
+    int mode = switching ? 1 : 0;
     for (int launch = 0;; ++launch) {
         a.phase_init = launch == 0 ? 1 : 0;
         a.trace_k0 = hctl.k + 1;
-        if (switching && launch >= 64) launch_version = 4;  // pathological oscillation
+        if (switching && launch >= 64) mode = 0;  // pathological oscillation
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
-        cuda_ok(launch_run(prec, labels, a, st, launch_version), "ptp_run_kernel launch");
+        cuda_ok(launch_run(prec, labels, a, st, mode), "ptp_run_kernel launch");
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         cuda_ok(cudaMemcpyAsync(&hctl, ws.ctl, sizeof(GroupCtl), cudaMemcpyDeviceToHost, st),
                 "read state");
@@ -511,6 +507,13 @@ void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, mh->ev0, mh->ev1);
         total_ms += ms;
+        if (hctl.err >= 2) {
+            // a CTA's claim list overflowed (the kernel stopped the field): redo it
+            // with lists that cannot overflow, before any observer call sees it
+            ws.grow_claims();
+            run_solve(mh, q);
+            return;
+        }
         if (want_trace && q.trace) {
             const int got = hctl.k - a.trace_k0 + 1;
             if (got > 0) {
@@ -531,19 +534,14 @@ void run_solve(geodist_mesh_s* mh, const Solve& q, int version) {
         }
         if (hctl.done) break;
         if (switching && hctl.mode_exit != 0) {
-            launch_version = hctl.mode_exit == 2 ? 6 : 5;
+            mode = hctl.mode_exit;
             continue;
         }
         if (chunk <= 0) throw Fail(GEODIST_ECUDA, "solver returned before convergence");
     }
     QueryStats qs{};
     cuda_ok(cudaMemcpy(&qs, a.qstats, sizeof(QueryStats), cudaMemcpyDeviceToHost), "stats");
-    if (qs.pad >= 2 && version >= 3) {
-        // a CTA claimed more vertices in one iteration than its shared-memory
-        // list holds: redo the field with the general kernel
-        run_solve(mh, q, 2);
-        return;
-    }
+    if (qs.pad >= 2) throw Fail(GEODIST_ECUDA, "solver error " + std::to_string(qs.pad));
     if (a.dbg) {
         std::vector<unsigned long long> h(kDbgSlots * static_cast<size_t>(a.dbg_iters) * maxb);
         cuda_ok(cudaMemcpy(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost), "dbg");
@@ -825,7 +823,7 @@ int geodist_toplesets(geodist_mesh_t mesh, const int32_t* sources, int32_t m, in
         cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
         const int n = mh->n;
         const int maxb = std::max(1, topo_max_blocks(mh->device));
-        mh->ws.ensure(1, n, run_max_blocks(0, false, mh->device));
+        mh->ws.ensure(1, n, run_max_blocks(0, false, mh->device, 0));
         if (!mh->t_sorted) {
             mh->t_sorted = dalloc<int>(n);
             mh->t_position = dalloc<int>(n);
@@ -894,6 +892,54 @@ int geodist_reorder_for_bands(geodist_mesh_t mesh, const int32_t* sources, int32
     });
 }
 
+int geodist_reorder_ordered(geodist_mesh_t mesh, const int32_t* sorted, int32_t reachable,
+                            const int32_t* position, int32_t* old_of_new, int32_t* new_of_old,
+                            int32_t* faces_out, double* xyz_out) {
+    return guarded([&] {
+        auto* mh = M(mesh);
+        std::lock_guard<std::mutex> lock(mh->mu);
+        const int n = mh->n, nf = mh->nf;
+        if (reachable < 0 || reachable > n || (reachable > 0 && !sorted) || !position)
+            throw std::invalid_argument("reorder_for_bands: ordering built for a different mesh");
+        // the ordering must be a partial permutation: position[sorted[p]] == p, and
+        // exactly `reachable` vertices have a position (toplesets.hpp:16-28)
+        int have = 0;
+        for (int v = 0; v < n; ++v) have += position[v] >= 0;
+        bool ok = have == reachable;
+        for (int p = 0; ok && p < reachable; ++p)
+            ok = sorted[p] >= 0 && sorted[p] < n && position[sorted[p]] == p;
+        if (!ok) throw std::invalid_argument("reorder_for_bands: ordering built for a different mesh");
+        if (xyz_out && !mh->has_geometry)
+            throw Fail(GEODIST_EINVAL, "mesh was created without vertex positions (topology only)");
+        cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
+        std::unique_ptr<void, DFree> srt(dalloc<int>(std::max(reachable, 1))), pos(dalloc<int>(n)),
+            oon(dalloc<int>(n)), noo(dalloc<int>(n)), fo(dalloc<int>(3 * static_cast<size_t>(nf))),
+            xo(xyz_out ? dalloc<double>(3 * static_cast<size_t>(n)) : nullptr);
+        cudaStream_t st = mh->stream;
+        if (reachable)
+            cuda_ok(cudaMemcpyAsync(srt.get(), sorted, sizeof(int) * reachable,
+                                    cudaMemcpyHostToDevice, st), "h2d");
+        cuda_ok(cudaMemcpyAsync(pos.get(), position, sizeof(int) * n, cudaMemcpyHostToDevice, st),
+                "h2d");
+        cuda_ok(launch_reorder(static_cast<int*>(pos.get()), static_cast<int*>(srt.get()),
+                               reachable, n, mh->faces, nf, static_cast<int*>(oon.get()),
+                               static_cast<int*>(noo.get()), static_cast<int*>(fo.get()), st,
+                               xyz_out ? mh->xyz : nullptr, static_cast<double*>(xo.get())),
+                "reorder");
+        cuda_ok(cudaStreamSynchronize(st), "reorder");
+        if (old_of_new)
+            cuda_ok(cudaMemcpy(old_of_new, oon.get(), sizeof(int) * n, cudaMemcpyDeviceToHost), "d2h");
+        if (new_of_old)
+            cuda_ok(cudaMemcpy(new_of_old, noo.get(), sizeof(int) * n, cudaMemcpyDeviceToHost), "d2h");
+        if (faces_out)
+            cuda_ok(cudaMemcpy(faces_out, fo.get(), sizeof(int) * 3 * nf, cudaMemcpyDeviceToHost),
+                    "d2h");
+        if (xyz_out)
+            cuda_ok(cudaMemcpy(xyz_out, xo.get(), sizeof(double) * 3 * n, cudaMemcpyDeviceToHost),
+                    "d2h");
+    });
+}
+
 int geodist_ptp(geodist_mesh_t mesh, const int32_t* sources, int32_t m,
                 const geodist_ptp_config* config, double* distances, int32_t* labels,
                 geodist_ptp_stats* stats, geodist_band_row* trace, int32_t trace_cap,
@@ -936,6 +982,11 @@ int geodist_ptp_ordered(geodist_mesh_t mesh, const int32_t* sources, int32_t m,
             throw std::invalid_argument("ptp_run: ordering does not match the source set");
         if (!position || reachable < 0 || reachable > mh->n || limits[rho] != reachable)
             throw std::invalid_argument("ptp_run: ordering built for a different mesh");
+        // the kernel indexes positions and packed records through limits: it must be a
+        // non-decreasing sequence inside [0, reachable]
+        for (int r = 0; r < rho; ++r)
+            if (limits[r] < 0 || limits[r] > limits[r + 1])
+                throw std::invalid_argument("ptp_run: ordering built for a different mesh");
         for (int q = 0; q < m; ++q) {
             const int s = sources[q];
             if (s < 0 || s >= mh->n || position[s] == -1 || position[s] >= limits[1])
@@ -993,10 +1044,11 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
         const int prec = config->precision;
         mh->ensure_prec(prec);
-        int version = solver_version();
     fps_retry:
-        const int maxb = std::min(run_max_blocks(prec, true, mh->device, version),
-                                  run_max_blocks(prec, false, mh->device, version));
+        int maxb = INT_MAX;
+        for (int md = 0; md < 3; ++md)
+            maxb = std::min({maxb, run_max_blocks(prec, true, mh->device, md),
+                             run_max_blocks(prec, false, mh->device, md)});
         mh->ws.ensure(1, n, maxb);
         Workspace& ws = mh->ws;
         cudaStream_t st = mh->stream;
@@ -1033,20 +1085,16 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
             a.fps_final = s == count;
             a.out_labels = s == count ? static_cast<int*>(lab.get()) : nullptr;
             a.qstats = static_cast<QueryStats*>(hist.get()) + (s - 1);
-            if (version == 4) {
-                // no host round trip between rounds: a fixed launch sequence per round,
-                // narrow-only -> wide-only -> narrow-only -> combined, each resuming the
-                // field where the previous one handed it over (a launch whose field is
-                // complete returns at once)
-                for (int x = 0; x < 4; ++x) {
-                    a.phase_init = x == 0 ? 1 : 0;
-                    const int v = x == 3 ? 4 : (x & 1) ? 6 : 5;
-                    cuda_ok(launch_run(prec, s > 1, a, st, v), "fps round launch");
-                }
-                a.phase_init = 1;
-            } else {
-                cuda_ok(launch_run(prec, s > 1, a, st, version), "fps round launch");
+            // no host round trip between rounds: a fixed launch sequence per round,
+            // narrow-only -> wide-only -> narrow-only -> combined, each resuming the
+            // field where the previous one handed it over (a launch whose field is
+            // complete returns at once)
+            for (int x = 0; x < 4; ++x) {
+                a.phase_init = x == 0 ? 1 : 0;
+                const int md = x == 3 ? 0 : (x & 1) ? 2 : 1;
+                cuda_ok(launch_run(prec, s > 1, a, st, md), "fps round launch");
             }
+            a.phase_init = 1;
         }
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         cuda_ok(cudaStreamSynchronize(st), "fps");
@@ -1057,9 +1105,8 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         cuda_ok(cudaMemcpy(hs.data(), d_samples, sizeof(int) * count, cudaMemcpyDeviceToHost), "d2h");
         cuda_ok(cudaMemcpy(hh.data(), hist.get(), sizeof(QueryStats) * count,
                            cudaMemcpyDeviceToHost), "d2h");
-        if (version >= 3 && std::any_of(hh.begin(), hh.end(),
-                                        [](const QueryStats& x) { return x.pad >= 2; })) {
-            version = 2;  // claim-list overflow: redo the sampling on the general kernel
+        if (std::any_of(hh.begin(), hh.end(), [](const QueryStats& x) { return x.pad >= 2; })) {
+            ws.grow_claims();  // claim-list overflow: redo the sampling with full-size lists
             goto fps_retry;
         }
         for (int s = 1; s < count; ++s)
@@ -1138,9 +1185,10 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         const int prec = config->precision;
         mh->ensure_prec(prec);
         const int n = mh->n;
-        int version = solver_version();
     batch_retry:
-        const int maxb = run_max_blocks(prec, multi, mh->device, version);
+        int maxb = INT_MAX;
+        for (int md = 0; md < 3; ++md)
+            maxb = std::min(maxb, run_max_blocks(prec, multi, mh->device, md));
         int g = groups > 0 ? groups : std::min(nq, 4);
         g = std::max(1, std::min({g, nq, maxb}));
         const int bpg = maxb / g;
@@ -1179,15 +1227,15 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         a.out_labels = config->with_labels ? out_labels : nullptr;
         a.qstats = static_cast<QueryStats*>(qs.get());
         float ms_sync = -1.f;  // device time when the launches were timed one by one
-        if (version == 4 && g == 1 && nq == 1) {
+        if (g == 1 && nq == 1) {
             // one field: narrow-only first, the other mode only if the field hands over
             // (host-read state; no launches that would return at once)
             ms_sync = 0.f;
-            int v = 5;
+            int md = 1;
             for (int launch = 0; launch < 64; ++launch) {
                 a.phase_init = launch == 0 ? 1 : 0;
                 cuda_ok(cudaEventRecord(mh->ev0, st), "event");
-                cuda_ok(launch_run(prec, multi, a, st, launch >= 63 ? 4 : v), "batch launch");
+                cuda_ok(launch_run(prec, multi, a, st, launch >= 63 ? 0 : md), "batch launch");
                 cuda_ok(cudaEventRecord(mh->ev1, st), "event");
                 GroupCtl hc{};
                 cuda_ok(cudaMemcpyAsync(&hc, ws.ctl, sizeof(GroupCtl), cudaMemcpyDeviceToHost, st),
@@ -1196,14 +1244,14 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
                 float ms1 = 0.f;
                 cudaEventElapsedTime(&ms1, mh->ev0, mh->ev1);
                 ms_sync += ms1;
-                if (hc.done || hc.mode_exit == 0) break;
-                v = hc.mode_exit == 2 ? 6 : 5;
+                if (hc.done || hc.mode_exit == 0 || hc.err >= 2) break;
+                md = hc.mode_exit;
             }
         }
         cuda_ok(cudaEventRecord(mh->ev0, st), "event");
         if (ms_sync >= 0.f) {
             // launched and timed above
-        } else if (version == 4 && g == 1) {
+        } else if (g == 1) {
             // one field at a time on the whole GPU (wide-band meshes): the narrow/wide
             // launch sequence per query, enqueued without host round trips
             const size_t esz = prec == GEODIST_DOUBLE ? 8 : 4;
@@ -1216,21 +1264,20 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
                 a.qstats = static_cast<QueryStats*>(qs.get()) + q;
                 for (int x = 0; x < 4; ++x) {
                     a.phase_init = x == 0 ? 1 : 0;
-                    const int v = x == 3 ? 4 : (x & 1) ? 6 : 5;
-                    cuda_ok(launch_run(prec, multi, a, st, v), "batch launch");
+                    const int md = x == 3 ? 0 : (x & 1) ? 2 : 1;
+                    cuda_ok(launch_run(prec, multi, a, st, md), "batch launch");
                 }
             }
         } else {
-            cuda_ok(launch_run(prec, multi, a, st, version), "batch launch");
+            cuda_ok(launch_run(prec, multi, a, st, 0), "batch launch");
         }
         cuda_ok(cudaEventRecord(mh->ev1, st), "event");
         std::vector<QueryStats> hq(nq);
         cuda_ok(cudaMemcpyAsync(hq.data(), qs.get(), sizeof(QueryStats) * nq,
                                 cudaMemcpyDeviceToHost, st), "d2h");
         cuda_ok(cudaStreamSynchronize(st), "batch");
-        if (version >= 3 &&
-            std::any_of(hq.begin(), hq.end(), [](const QueryStats& x) { return x.pad >= 2; })) {
-            version = 2;
+        if (std::any_of(hq.begin(), hq.end(), [](const QueryStats& x) { return x.pad >= 2; })) {
+            ws.grow_claims();  // claim-list overflow: redo the batch with full-size lists
             goto batch_retry;
         }
         float ms = 0.f;

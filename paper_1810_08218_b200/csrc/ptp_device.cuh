@@ -38,10 +38,8 @@ constexpr int kMetaShift = 27;     // entry 0 bits 27..30 hold the corner count 
 constexpr int kIdMask = (1 << kMetaShift) - 1;
 constexpr int kEllOverflow = 15;   // d code: more than 7 corners, use the CSR tables
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kWideFactor = 2;     // thread-per-vertex once the band exceeds 2x the CTA groups
-                                   // (RunArgs.wide_factor; GEODIST_WIDE overrides)
-constexpr int kSlotsPerLane = 8;       // v3: barrier payload slots read per lane of warp 0
-constexpr int kMaxGroupBlocks = 32 * kSlotsPerLane;  // v3: CTAs per query group
+constexpr int kWideFactor = 2;     // RunArgs.wide_factor default (GEODIST_WIDE=0 forces the
+                                   // wide path on every iteration: tests)
 
 // ELL entry e of a vertex lives at slot (e % 4) * 2 + e / 4, so lane l of a
 // 4-lane group reads entries l and l + 4 as one 8-byte (or 16-byte) vector.
@@ -136,22 +134,13 @@ struct RunArgs {
     // (work start, work end after the CTA reduction, barrier release)
     unsigned long long* dbg;
     int dbg_iters;
-    // v3 (claimer-first) solver: BFS-ordered packed records by queue position
+    // packed records by BFS position (slot-major: slot s of position p at s * stride + p)
     int* pring;          // 8 ints per position (ELL interleaved)
     void* pL;            // 8 T per position
     void* pquad;         // 8 Quad<T> per position
-    unsigned long long* blk_slot;  // [2][gridDim.x][2]: max-rel bits, claim count
-    int wide_factor;     // v2: band > wide_factor * CTA groups -> one thread per vertex
-    int* blists;         // [2][gridDim.x][claim_cap] per-CTA claim lists
+    int wide_factor;     // 0 forces the wide (one vertex per thread) path on every iteration
+    int* blists;         // [gridDim.x][claim_cap] per-CTA claim lists (beyond the smem list)
     int claim_cap;       // capacity of one claim list
-    int cache_slots;     // v4: shared-memory record cache slots per CTA
-    int mode;            // v4 launch mode: 0 combined, 1 narrow bands only, 2 wide bands only
-};
-
-// Per-CTA barrier payload slot (16 B): max relative change bits and claims.
-struct alignas(16) BlkSlot {
-    unsigned long long maxbits;
-    unsigned long long count;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -21,15 +21,16 @@ void launch_planar_test(int precision, const double* x1, const double* x2, const
 void launch_arith_selftest(long long n, unsigned long long seed, unsigned long long* out,
                            cudaStream_t st);
 
+// The solver (ptp_run4.cu) in three instantiations: mode 0 handles every iteration,
+// mode 1 narrow-band iterations only, mode 2 wide-band iterations only (each hands
+// the field to the other at a band cross-over, GroupCtl.mode_exit).
 // Max co-resident CTAs of the run kernel on `device` (cooperative launch bound).
-// version 3: claimer-first solver (default); version 2: general queue-based solver
-// (used when a CTA's claims overflow its shared-memory list).
-int run_max_blocks(int precision, bool labels, int device, int version = 3);
-// v4 (ptp_run4.cu): record-cache bytes (dynamic shared memory) and kernel entry
+int run_max_blocks(int precision, bool labels, int device, int mode = 0);
+// record-cache bytes (dynamic shared memory) and kernel entry
 size_t run4_dyn_smem(int precision, bool labels);
 const void* run4_kernel_ptr(int precision, bool labels, int mode = 0);
 cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st,
-                       int version = 3);
+                       int mode = 0);
 
 // Toplesets with the reference's exact ordering (toplesets.cu).
 struct TopoArgs {
@@ -52,9 +53,11 @@ cudaError_t launch_toplesets(const TopoArgs& a, int* scratch, size_t scratch_wor
                              cudaStream_t st);
 
 // reorder_for_bands: old_of_new / new_of_old / permuted faces (toplesets.cu).
+// xyz / xyz_out: optional position permutation (xyz_out[p] = xyz[old_of_new[p]]).
 cudaError_t launch_reorder(const int* position, const int* sorted, int reachable, int n,
                            const int* faces, int nf, int* old_of_new, int* new_of_old,
-                           int* faces_out, cudaStream_t st);
+                           int* faces_out, cudaStream_t st, const double* xyz = nullptr,
+                           double* xyz_out = nullptr);
 
 // On-device fan-CSR build (mesh_build.cu).  Returns 0 for a valid mesh, else the
 // validation flag bits (~0u with *err set on a CUDA error).

@@ -616,9 +616,14 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             }
             const int cnt = static_cast<int>(payload >> 32);
             if (cnt > 0) {
+                // claims beyond the lists' capacity were dropped (err 2: the field is
+                // abandoned at this barrier and redone with larger lists); their
+                // positions get vertex 0, an in-bounds placeholder
                 const int at = level_start + static_cast<int>(__shfl_sync(kFull, old, 0) >> 32);
                 for (int x = tid; x < cnt; x += 32)
-                    pv[at + x] = x < kSmemClaims ? s_list[x] : g_list[x - kSmemClaims];
+                    pv[at + x] = x < kSmemClaims           ? s_list[x]
+                                 : x - kSmemClaims < A.claim_cap ? g_list[x - kSmemClaims]
+                                                                 : 0;
             }
             if (tid == 0) {
                 unsigned long long x = old + payload + 1ull;
@@ -632,6 +637,17 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         }
         ++bseq;
         __syncthreads();
+    };
+
+    // A CTA whose claim list overflowed (s_err 2) or whose new position was never
+    // written (3) adds nb + 1 to the barrier word's nonconverged-CTA field (bits
+    // 16-31, at most nb <= 255 otherwise): every CTA of the group then sees the
+    // same word and ends the field (the host redoes it; the err reaches ctl->err).
+    auto abort_bits = [&]() -> unsigned long long {
+        return s_err >= 2 ? static_cast<unsigned long long>(nb + 1) << 16 : 0ull;
+    };
+    auto aborted = [&](unsigned long long x) {
+        return static_cast<int>((x >> 16) & 0xffffull) > nb;
     };
 
     // reset the record cache tags (smem does not survive launches)
@@ -803,7 +819,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 }
                 __syncthreads();
                 const unsigned long long cnt = static_cast<unsigned long long>(s_ccnt);
-                barrier(cnt << 32, m, [] {}, [&](unsigned long long x) {
+                barrier((cnt << 32) | abort_bits(), m, [] {}, [&](unsigned long long x) {
                     const int tot = static_cast<int>(x >> 32);
                     bb = m;
                     set_lim(0, 0);
@@ -821,7 +837,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         set_lim(2, tail);
                         if (lb == 0) limits[2] = tail;
                     }
-                    done = !bfs_open && i > rho - 1;
+                    done = (!bfs_open && i > rho - 1) || aborted(x);
                     shares_now();
                     publish();
                 });
@@ -1050,8 +1066,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 if (tid == 0 && bmax > T(0)) atomicMax(&ctl->slot[kk % 3], Lim<T>::bits(bmax));
             }
             if (dbg) dslot[1] = gtimer();
-            const unsigned long long pay =
-                (nonconv ? (1ull << 16) : 0ull) | (static_cast<unsigned long long>(s_ccnt) << 32);
+            const unsigned long long pay = (nonconv ? (1ull << 16) : 0ull) | abort_bits() |
+                                           (static_cast<unsigned long long>(s_ccnt) << 32);
             int c_p0 = 0, c_a0 = 0, n_p0 = 0, n_a0 = 0, c_nfz = 0;
             barrier(pay, be_, [&] {
                 first_owned(fe, c_p0, c_a0);  // converged: the band starts at fe
@@ -1059,7 +1075,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 c_nfz = owned_count(n_p0, fe);  // converged: [bb, fe) is frozen next
             }, [&](unsigned long long x) {
                 if (dbg) dslot[2] = gtimer();
-                const int nnc = static_cast<int>((x >> 16) & 0xffffull);
+                const int nnc = static_cast<int>((x >> 16) & 0xffffull);  // <= nb unless aborted
                 const int tot = static_cast<int>(x >> 32);
                 const bool conv = nnc == 0;  // ptp.cpp:114
                 const int ub = bb, ue = be_pub;
@@ -1101,7 +1117,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 tail = nt;
                 parity ^= 1;
                 k = kk;
-                done = !bfs_open && i > rho - 1;
+                done = (!bfs_open && i > rho - 1) || aborted(x);
                 publish();
                 if (dbg) dslot[8] = gtimer();
             }, true);

@@ -283,9 +283,16 @@ __global__ void relabel_kernel(const int* new_of_old, const int* faces, long lon
         faces_out[x] = new_of_old[faces[x]];
 }
 
+__global__ void permute_xyz_kernel(const int* old_of_new, int n, const double* xyz,
+                                   double* xyz_out) {
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < 3LL * n;
+         x += (long long)gridDim.x * blockDim.x)
+        xyz_out[x] = xyz[3LL * old_of_new[x / 3] + x % 3];
+}
+
 cudaError_t launch_reorder(const int* position, const int* sorted, int reachable, int n,
                            const int* faces, int nf, int* old_of_new, int* new_of_old,
-                           int* faces_out, cudaStream_t st) {
+                           int* faces_out, cudaStream_t st, const double* xyz, double* xyz_out) {
     cudaError_t e = cudaMemcpyAsync(old_of_new, sorted, sizeof(int) * reachable,
                                     cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
@@ -296,6 +303,10 @@ cudaError_t launch_reorder(const int* position, const int* sorted, int reachable
     note_launch();
     relabel_kernel<<<1184, 256, 0, st>>>(new_of_old, faces, 3LL * nf, faces_out);
     note_launch();
+    if (xyz && xyz_out) {
+        permute_xyz_kernel<<<1184, 256, 0, st>>>(old_of_new, n, xyz, xyz_out);
+        note_launch();
+    }
     return cudaGetLastError();
 }
 

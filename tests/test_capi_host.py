@@ -112,3 +112,30 @@ def test_compute_fails_loudly_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(RuntimeError, match="CUDA"):
         g.generate_icosphere(1)
+
+
+@pytest.mark.parametrize("kind", ["torus", "noisy_icosphere", "heightfield"])
+def test_synthetic_generators_equal_reference_side_generators(kind):
+    """The bench's reference arm builds its meshes with oracle/ref_capi.cpp's generators
+    (reference types, no product library): they must give the product's arrays bit for bit."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    if kind == "torus":
+        R, (v, f) = ref.RefMesh.torus(57, 31), g.torus_arrays(57, 31)
+    elif kind == "noisy_icosphere":
+        R, (v, f) = ref.RefMesh.noisy_icosphere(4, 2e-3, 1), g.noisy_icosphere_arrays(4, 2e-3, 1)
+    else:
+        R, (v, f) = ref.RefMesh.heightfield(65, 33), g.heightfield_arrays(65, 33)
+    rv, rf = R.arrays()
+    assert np.array_equal(rv.view(np.int64), v.view(np.int64))
+    assert np.array_equal(rf, f)
+
+
+def test_source_index_beyond_int32_rejected():
+    """an int64 source index must not wrap onto another vertex."""
+    with pytest.raises(ValueError, match="out of range"):
+        g._sources([2 ** 32])
+    with pytest.raises(ValueError, match="out of range"):
+        g._sources([0, -2 ** 40])
+    assert g._sources([5, 7]).dtype == np.int32

@@ -15,13 +15,11 @@ import paper_1810_08218_b200 as g
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["v4", "v4-wide", "v3", "v2", "v2-wide"], autouse=True)
+@pytest.fixture(params=["v4", "v4-wide"], autouse=True)
 def solver(request, monkeypatch):
-    """Run every parity test on all solver paths: the owner-cached kernel (v4, default)
-    and its thread-per-vertex wide-band path forced on every iteration (v4-wide), the
-    queue-based kernel (v2) and its wide path (v2-wide), and the claimer-first kernel
-    with BFS-ordered packed records (v3)."""
-    monkeypatch.setenv("GEODIST_SOLVER", request.param[1])
+    """Run every parity test on both relaxation paths of the solver: the default
+    narrow/wide hand-over (v4) and the thread-per-vertex wide-band path forced on
+    every iteration (v4-wide)."""
     if request.param.endswith("-wide"):
         monkeypatch.setenv("GEODIST_WIDE", "0")
     else:
@@ -88,6 +86,13 @@ def test_reorder_for_bands_exact(name):
     assert np.array_equal(oon, gd["old_of_new"])
     assert np.array_equal(noo, gd["new_of_old"])
     assert np.array_equal(P.faces(), gd["reordered_faces"])
+    # the caller-ordering entry point (the drop-in's): same permutation, positions
+    # permuted on the device
+    o = {"sorted": gd["sorted"], "position": gd["position"]}
+    P2, oon2, noo2 = g.reorder_for_bands(M, ordering=o)
+    assert np.array_equal(oon2, gd["old_of_new"]) and np.array_equal(noo2, gd["new_of_old"])
+    assert np.array_equal(P2.faces(), gd["reordered_faces"])
+    assert np.array_equal(bits(P2.vertices()), bits(np.asarray(gd["vertices"])[oon2]))
     # test_ptp.cpp:159-180: results bit-identical after un-permutation
     labels = "labels_d" in gd
     src = noo[gd["sources"]]
@@ -151,6 +156,10 @@ SYNTH = [
     ("wheel23", lambda: polar_arrays(23, 6), [[0], [3]]),
     # 5000 claims by one CTA in one iteration: the on-chip claim list spills to global
     ("wheel5000", lambda: polar_arrays(5000, 3), [[0], [7, 12000]]),
+    # 9000 claims by one CTA in one iteration: beyond the CTA's global list as first
+    # sized, so the field is abandoned (err 2) and redone with full-size lists; from
+    # the centre (iteration-0 claims) and from a spoke (the centre claims at k = 1)
+    ("wheel9000", lambda: polar_arrays(9000, 3), [[0], [7], [7, 20000]]),
     ("ico5", lambda: g.icosphere_arrays(5), [[0], [5, 700, 9000]]),
     ("noisy_ico6", lambda: g.noisy_icosphere_arrays(6, 2e-3, 1), [[0], [1, 20000, 33333, 40000]]),
     ("torus64x48", lambda: g.torus_arrays(64, 48), [[0], [17, 1500, 3000]]),
@@ -175,6 +184,23 @@ def test_synthetic_vs_restatement(port_lib, name, make, sources):
             assert got["iterations"] == want["iterations"]
             assert got["relax_calls"] == want["relax_calls"]
             assert got["degenerate_calls"] == want["degenerate_calls"]
+
+
+def test_claim_overflow_batch_and_fps_redo(port_lib):
+    """The claim-list overflow redo on the batch and FPS entry points: a
+    9000-spoke wheel, fields equal the single-field path / the restatement."""
+    v, f = polar_arrays(9000, 3)
+    M = g.Mesh(v, f)
+    queries = [[0], [7], [9001, 18000]]
+    out = g.batch_geodesics(M, queries, precision="single", labels=True, groups=2)
+    for q, src in enumerate(queries):
+        one = g.geodesics(M, src, precision="single", labels=True)
+        assert np.array_equal(bits(out["distances"][q]), bits(one["distances"]))
+        assert np.array_equal(out["labels"][q], one["labels"])
+    r = g.farthest_point_sampling(M, 4, seed=7)
+    want = port_lib.PortMesh(v, f).fps(4, seed=7)
+    assert list(r["samples"]) == list(want["samples"])
+    assert np.array_equal(r["labels"], want["labels"])
 
 
 def test_batch_equals_single_runs():
@@ -339,3 +365,20 @@ def test_fps_across_handover_parity():
     assert list(got["samples"]) == list(want["samples"])
     assert np.array_equal(got["labels"], want["labels"])
     assert got["radius"] == want["radius"]
+
+
+def test_malformed_orderings_rejected():
+    """ptp_run / reorder_for_bands with an ordering that is not one of this
+    mesh's (decreasing limits, a position array inconsistent with sorted) fail with the
+    reference's invalid_argument text instead of reaching device memory."""
+    v, f = g.icosphere_arrays(2)
+    M = g.Mesh(v, f)
+    t = g.toplesets(M, [0])
+    bad = {"sorted": t["sorted"], "limits": t["limits"].copy(), "position": t["position"]}
+    bad["limits"][2], bad["limits"][3] = bad["limits"][3], bad["limits"][2]
+    with pytest.raises(ValueError, match="ordering"):
+        g.geodesics_ordered(M, [0], bad)
+    pos = t["position"].copy()
+    pos[t["sorted"][3]] = 7
+    with pytest.raises(ValueError, match="ordering"):
+        g.reorder_for_bands(M, ordering={"sorted": t["sorted"], "position": pos})
