@@ -21,6 +21,7 @@
 
 #include "../../include/geodist_b200.h"
 #include "mesh_host.hpp"
+#include "ptp_common.cuh"
 #include "ptp_launch.hpp"
 
 namespace gdb {
@@ -105,10 +106,8 @@ void require_device(int device) {
 struct Workspace {
     int groups = 0;
     long long n = 0;
-    void* dist0 = nullptr;
-    void* dist1 = nullptr;
-    int* lab0 = nullptr;
-    int* lab1 = nullptr;
+    void* cell0 = nullptr;  // Jacobi double buffer: Cell<T, LABELS> (<= 16 B) per vertex
+    void* cell1 = nullptr;
     int* level = nullptr;
     int* queue = nullptr;
     int* limits = nullptr;
@@ -122,7 +121,7 @@ struct Workspace {
     int claim_cap = 0;
     int claim_min = 0;                     // raised after a claim-list overflow
 
-    // dist0/dist1/lab0/lab1/level/queue live in one block (`hot`): the per-vertex
+    // cell0/cell1/level/queue live in one block (`hot`): the per-vertex
     // arrays every iteration gathers from.  Solver launches mark it L2-persisting so
     // the streaming reads of ELL rows (one per vertex, ~n * 192 B per field) do not
     // evict the distance and level lines of the vertices the wavefront reaches next.
@@ -156,14 +155,12 @@ struct Workspace {
         const size_t e = static_cast<size_t>(g) * static_cast<size_t>(nn);
         {
             auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
-            const size_t b8 = up(e * sizeof(double)), b4 = up(e * sizeof(int));
-            hot_bytes = 2 * b8 + 4 * b4;
+            const size_t bc = up(e * kCellMaxBytes), b4 = up(e * sizeof(int));
+            hot_bytes = 2 * bc + 2 * b4;
             hot = dalloc<char>(hot_bytes);
             char* x = hot;
-            dist0 = x; x += b8;
-            dist1 = x; x += b8;
-            lab0 = reinterpret_cast<int*>(x); x += b4;
-            lab1 = reinterpret_cast<int*>(x); x += b4;
+            cell0 = x; x += bc;
+            cell1 = x; x += bc;
             level = reinterpret_cast<int*>(x); x += b4;
             queue = reinterpret_cast<int*>(x);
         }
@@ -213,10 +210,8 @@ struct Workspace {
     void fill(RunArgs& a) const {
         const char* w = getenv("GEODIST_WIDE");
         a.wide_factor = w ? atoi(w) : kWideFactor;
-        a.dist0 = dist0;
-        a.dist1 = dist1;
-        a.lab0 = lab0;
-        a.lab1 = lab1;
+        a.cell0 = cell0;
+        a.cell1 = cell1;
         a.level = level;
         a.queue = queue;
         a.limits = limits;
@@ -526,10 +521,12 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
         if (stepwise && hctl.k >= a.trace_k0) {
             // IterationObserver: snapshot of dist[curr] after iteration k (ptp.cpp:118-120);
             // the buffer written last is the one the saved parity names.
-            const void* buf = hctl.parity ? ws.dist1 : ws.dist0;
+            const void* buf = hctl.parity ? ws.cell1 : ws.cell0;
             snap.resize(n);
-            cuda_ok(cudaMemcpy(snap.data(), buf, sizeof(double) * n, cudaMemcpyDeviceToHost),
-                    "snapshot");
+            // the distance is the first 8 bytes of each fp64 cell
+            const size_t pitch = labels ? sizeof(Cell<double, true>) : sizeof(Cell<double, false>);
+            cuda_ok(cudaMemcpy2D(snap.data(), sizeof(double), buf, pitch, sizeof(double), n,
+                                 cudaMemcpyDeviceToHost), "snapshot");
             q.observer(q.observer_user, hctl.k, snap.data(), n);
         }
         if (hctl.done) break;

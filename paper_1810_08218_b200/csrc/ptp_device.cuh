@@ -11,8 +11,9 @@
 //                        (update_kernel.hpp:55-60), computed in T with the
 //                        reference's operation order (no FMA)
 // Per query (per group of CTAs):
-//   dist0/dist1<T>[n]    Jacobi double buffer (ptp.cpp:61-63), original order
-//   lab0/lab1[n]         nearest-source labels (multi-source runs only)
+//   cell0/cell1[n]       Jacobi double buffer (ptp.cpp:61-63), original order:
+//                        Cell<T, LABELS> = distance (+ nearest-source label for
+//                        multi-source runs) + change stamp (ptp_common.cuh)
 //   level[n]             BFS level (-1 = unvisited), fused topleset discovery
 //   queue[n]             vertices in BFS order, level r at [limits[r], limits[r+1])
 //   limits[n+2]
@@ -94,10 +95,8 @@ struct MeshDev {
 struct RunArgs {
     MeshDev mesh;
     // per-group buffers: group g at base + g * stride (elements)
-    void* dist0;
-    void* dist1;
-    int* lab0;
-    int* lab1;
+    void* cell0;         // Cell<T, LABELS>[stride] per group
+    void* cell1;
     int* level;
     int* queue;
     int* limits;

@@ -155,8 +155,8 @@ template <typename T, bool LABELS>
 __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
                                        int sl, bool act, bool is_new, bool cached, bool pack,
                                        int p, int kk, const int* pv, const int* pring, const T* pL,
-                                       const char* pquad, const T* dp, T* dc, const int* lp,
-                                       int* lc, int fe, bool expand, int* level, T eps,
+                                       const char* pquad, const Cell<T, LABELS>* cp,
+                                       Cell<T, LABELS>* cc, int fe, bool expand, int* level, T eps,
                                        const ClaimCtx& CC, int& nonconv, T& my_max,
                                        long long& calls, long long& degs, bool& ca_claim,
                                        int& ida, bool& cb_claim, int& idb,
@@ -261,20 +261,24 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     ca_claim = false;
     cb_claim = false;
     T tv = inf;
-    int lv = -1;
+    int lv = -1, sv = 0;
     T ta = inf, tb = inf;
     int la = -1, lb_ = -1;
     if (act && gl == 0) {
-        tv = ldcg(dp + v);
-        if (LABELS) lv = ldcg(lp + v);
+        const Cell<T, LABELS> c = ld_cell(cp + v);
+        tv = c.d;
+        lv = c.lab();
+        sv = c.stamp();
     }
     if (hasa) {
-        ta = ldcg(dp + ida);
-        if (LABELS) la = ldcg(lp + ida);
+        const Cell<T, LABELS> c = ld_cell(cp + ida);
+        ta = c.d;
+        la = c.lab();
     }
     if (hasb) {
-        tb = ldcg(dp + idb);
-        if (LABELS) lb_ = ldcg(lp + idb);
+        const Cell<T, LABELS> c = ld_cell(cp + idb);
+        tb = c.d;
+        lb_ = c.lab();
     }
     // BFS claims (toplesets.cpp:44-52), issued after the distance loads: an atomic
     // ahead of them in the memory pipeline would delay the loads
@@ -332,12 +336,14 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                 if (hb) cB = atomicCAS(level + ib, -1, kk + 1) == -1;
             }
             if (ha) {
-                TA = ldcg(dp + ia);
-                if (LABELS) lA = ldcg(lp + ia);
+                const Cell<T, LABELS> c = ld_cell(cp + ia);
+                TA = c.d;
+                lA = c.lab();
             }
             if (hb) {
-                TB = ldcg(dp + ib);
-                if (LABELS) lB = ldcg(lp + ib);
+                const Cell<T, LABELS> c = ld_cell(cp + ib);
+                TB = c.d;
+                lB = c.lab();
             }
             const int dlim = act && ovf ? min(d, base + kEllW - 1) : 0;
             chunk_candidates<T, LABELS>(gl, base, dlim, xa, xb, LA, LB, TA, TB, lA, lB, QA, QB,
@@ -359,8 +365,9 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
         }
     }
     if (act && gl == 0) {
-        dc[v] = best;
-        if (LABELS) lc[v] = blab;
+        // the change stamp: this iteration if the distance changed (a label changes
+        // only with its distance, update_kernel.hpp:114-117)
+        st_cell(cc + v, make_cell<T, LABELS>(best, blab, best != tv ? kk : sv));
         calls += d;
         if (p < fe || A.last_change != nullptr) {
             const T rc = rel_change(tv, best);
@@ -401,12 +408,27 @@ __device__ __forceinline__ void wide_pre(int p, size_t N, const int* pv, const i
     for (int e = 0; e < kEllW; ++e) w.raw[e] = __ldcg(pring + ell_slot(e) * N + p);
 }
 
+// Change-driven (multi-source runs, whose cells carry change stamps; ptp_common.cuh
+// Cell): the vertex is re-evaluated only over corners with an endpoint whose
+// distance changed in the previous iteration (stamp kk - 1).  relax_vertex is a pure
+// function of the neighbours' previous values and starts from the vertex's own
+// previous value, which is already <= every candidate of an unchanged corner, so
+// those corners can never be adopted (strict '<', update_kernel.hpp:114): skipping
+// them gives the same bits as evaluating them.  A vertex with no changed corner
+// keeps its value, and its cell is rewritten only if its value changed in this or
+// the previous iteration: otherwise both buffers already hold the same cell.  relax_calls and
+// degenerate_calls count every corner as the reference does: the degenerate test
+// (update_kernel.hpp:51-57 on finite, unmixed corners) is a function of the flags
+// and values already loaded.  |x| and the quads of the evaluated corners are loaded
+// after the stamps (a third trip for those only: the 2048^2 height field's band does
+// not fit L2, and the skipped loads are DRAM traffic).  Single-source runs evaluate
+// every corner with |x| and quads loaded together with the distances.
 template <typename T, bool LABELS>
 __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, int p, int kk,
                                             const WidePre& w, const T* pL, const char* pquad,
-                                            const T* dp, T* dc, const int* lp, int* lc, int fe,
-                                            T eps, int& nonconv, T& my_max, long long& calls,
-                                            long long& degs) {
+                                            const Cell<T, LABELS>* cp, Cell<T, LABELS>* cc,
+                                            int fe, T eps, int& nonconv, T& my_max,
+                                            long long& calls, long long& degs) {
     const T inf = Lim<T>::inf();
     const size_t N = static_cast<size_t>(A.stride);
     const int vr = w.vr;
@@ -425,26 +447,31 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
 #pragma unroll
         for (int e = 0; e < kEllW; ++e) raw[e] = __ldcg(M.ering + pb + ell_slot(e));
     }
-    const T tv = ldcg(dp + v);
-    const int lv = LABELS ? ldcg(lp + v) : -1;
+    constexpr bool kSkip = LABELS;
+    const Cell<T, LABELS> self = ld_cell(cp + v);
+    const T tv = self.d;
+    const int lv = self.lab();
+    const int prevk = kk - 1;
     int d = (raw[0] >> kMetaShift) & 15;
     T best = tv;
     int blab = lv;
     if (d == kEllOverflow) {
-        // more than 7 corners: CSR tables, sequential fan walk
+        // more than 7 corners: CSR tables, sequential fan walk, every corner evaluated
         const int c0 = __ldg(M.cptr + v);
         d = __ldg(M.cptr + v + 1) - c0;
         const int r0 = c0 + v;
         const T* ringL = static_cast<const T*>(M.ringL);
         int x0 = __ldg(M.ring + r0);
         int i0 = x0 & INT_MAX;
-        T t0 = ldcg(dp + i0), L0 = __ldg(ringL + r0);
-        int l0 = LABELS ? ldcg(lp + i0) : -1;
+        Cell<T, LABELS> n0 = ld_cell(cp + i0);
+        T t0 = n0.d, L0 = __ldg(ringL + r0);
+        int l0 = n0.lab();
         for (int c = 0; c < d; ++c) {
             const int x1 = __ldg(M.ring + r0 + c + 1);
             const int i1 = x1 & INT_MAX;
-            const T t1 = ldcg(dp + i1), L1 = __ldg(ringL + r0 + c + 1);
-            const int l1 = LABELS ? ldcg(lp + i1) : -1;
+            const Cell<T, LABELS> n1 = ld_cell(cp + i1);
+            const T t1 = n1.d, L1 = __ldg(ringL + r0 + c + 1);
+            const int l1 = n1.lab();
             Quad<T> q;
             q.load(M.quad, c0 + c);
             const bool mixed = LABELS && l0 != l1 && t0 != inf && t1 != inf;
@@ -463,24 +490,54 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
         constexpr int kQ = sizeof(T) == 4 ? kEllW : 1;
         T t[kEllW + 1], L[kEllW];
         int l[kEllW + 1];
+        bool ch[kEllW + 1];
         Quad<T> q[kQ];
 #pragma unroll
         for (int e = 0; e <= kEllW; ++e) {
             t[e] = inf;
             l[e] = -1;
+            ch[e] = false;
             if (e < kEllW) L[e] = T(0);
             if (e < kQ) q[e].q11 = q[e].q12 = q[e].q22 = q[e].a = T(0);
             if (e < kEllW && e <= d) {
-                t[e] = ldcg(dp + (raw[e] & kIdMask));
-                if (LABELS) l[e] = ldcg(lp + (raw[e] & kIdMask));
+                const Cell<T, LABELS> c = ld_cell(cp + (raw[e] & kIdMask));
+                t[e] = c.d;
+                l[e] = c.lab();
+                ch[e] = !kSkip || c.stamp() == prevk;
                 // fp64: |x| and the quads are loaded per corner pair below (registers)
-                if (sizeof(T) == 4) L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
-                if (sizeof(T) == 4 && e < kQ && e < d) q[e].load_cg(qsrc, pb + ell_slot(e) * step);
+                if (!kSkip && sizeof(T) == 4) L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
+                if (!kSkip && sizeof(T) == 4 && e < kQ && e < d)
+                    q[e].load_cg(qsrc, pb + ell_slot(e) * step);
+            }
+        }
+        if (kSkip && sizeof(T) == 4) {
+            // |x| and quads only for the corners that are evaluated (a third trip)
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e) {
+                const bool need_e = e <= d && ((e > 0 && (ch[e - 1] || ch[e])) ||
+                                               (e < d && (ch[e] || ch[e + 1])));
+                if (need_e) L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
+                if (e < kQ && e < d && (ch[e] || ch[e + 1])) q[e].load_cg(qsrc, pb + ell_slot(e) * step);
+            }
+        }
+        // degenerate corners (rare): counted whether or not they are evaluated
+        bool anydg = false;
+#pragma unroll
+        for (int c = 0; c < kEllW - 1; ++c) anydg |= c < d && raw[c] < 0;
+        if (anydg) {
+#pragma unroll
+            for (int c = 0; c < kEllW - 1; ++c) {
+                const bool mixed = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
+                degs += (c < d && raw[c] < 0 && t[c] != inf && t[c + 1] != inf && !mixed) ? 1 : 0;
             }
         }
 #pragma unroll
         for (int c = 0; c < kEllW - 1; c += 2) {
             if (c >= d) break;  // valence 6: three pairs, not four
+            // corners c (entries c, c+1) and c+1 (entries c+1, c+2)
+            const bool e0 = ch[c] || ch[c + 1];
+            const bool e1 = c + 1 < d && (ch[c + 1] || ch[c + 2]);
+            if (!(e0 || e1)) continue;
             const bool m0 = LABELS && l[c] != l[c + 1] && t[c] != inf && t[c + 1] != inf;
             const bool m1 = LABELS && l[c + 1] != l[c + 2] && t[c + 1] != inf && t[c + 2] != inf;
             T val[2];
@@ -492,45 +549,45 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
                 const Quad<float> qv[2] = {q[c % kQ], q[(c + 1) % kQ]};
                 const bool dgv[2] = {raw[c] < 0, raw[c + 1] < 0};
                 const bool mix[2] = {m0, m1};
-                const bool valid[2] = {c < d, c + 1 < d};
+                const bool valid[2] = {e0, e1};
                 corner_pair_f32(t1v, t2v, L1v, L2v, qv, dgv, mix, valid, val, side, deg);
             } else {
-                Quad<T> q0, q1;
-                q0.load_cg(qsrc, pb + ell_slot(c) * step);
-                const T L0 = ldcg(lsrc + pb + ell_slot(c) * step);
-                const T L1 = ldcg(lsrc + pb + ell_slot(c + 1) * step);
-                val[0] = corner_eval_f64<true>(t[c], t[c + 1], L0, L1, q0, raw[c] < 0, m0,
-                                               side[0], deg[0]);
-                if (c + 1 < d) {
+                val[0] = inf;
+                val[1] = inf;
+                side[0] = side[1] = -1;
+                if (e0) {
+                    Quad<T> q0;
+                    q0.load_cg(qsrc, pb + ell_slot(c) * step);
+                    const T L0 = ldcg(lsrc + pb + ell_slot(c) * step);
+                    const T L1 = ldcg(lsrc + pb + ell_slot(c + 1) * step);
+                    val[0] = corner_eval_f64<true>(t[c], t[c + 1], L0, L1, q0, raw[c] < 0, m0,
+                                                   side[0], deg[0]);
+                }
+                if (e1) {
+                    Quad<T> q1;
                     q1.load_cg(qsrc, pb + ell_slot(c + 1) * step);
+                    const T L1 = ldcg(lsrc + pb + ell_slot(c + 1) * step);
                     const T L2 = ldcg(lsrc + pb + ell_slot(c + 2 < kEllW ? c + 2 : c + 1) * step);
                     val[1] = corner_eval_f64<true>(t[c + 1], t[c + 2], L1, L2, q1,
                                                    raw[c + 1] < 0, m1, side[1], deg[1]);
-                } else {
-                    val[1] = inf;
-                    deg[1] = 0;
-                    side[1] = -1;
                 }
             }
-            if (!(c + 1 < d)) {
-                val[1] = inf;
-                deg[1] = 0;
-            }
-            degs += deg[0] + deg[1];
-            if (val[0] < best) {
+            if (e0 && val[0] < best) {
                 best = val[0];
                 if (LABELS) blab = side[0] == 0 ? l[c] : l[c + 1];
             }
-            if (c + 1 < d && val[1] < best) {
+            if (e1 && val[1] < best) {
                 best = val[1];
                 if (LABELS) blab = side[1] == 0 ? l[c + 1] : l[c + 2];
             }
         }
     }
-    dc[v] = best;
-    if (LABELS) lc[v] = blab;
     calls += d;
-    if (p < fe || A.last_change != nullptr) {
+    // The other buffer holds this vertex's cell of two iterations ago: rewrite it only
+    // if the value changed now or last iteration.
+    if (!kSkip || best != tv || self.stamp() == prevk)
+        st_cell(cc + v, make_cell<T, LABELS>(best, blab, best != tv ? kk : self.stamp()));
+    if (best != tv && (p < fe || A.last_change != nullptr)) {
         const T rc = rel_change(tv, best);
         if (p < fe && rc >= eps) nonconv = 1;
         if (p < fe && rc > my_max) my_max = rc;
@@ -569,12 +626,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
     GroupCtl* ctl = A.ctl + g;
     const long long off = static_cast<long long>(g) * A.stride;
     const long long off8 = off * kEllW;
-    T* dist[2] = {static_cast<T*>(A.dist0) + off, static_cast<T*>(A.dist1) + off};
-    int* lab[2] = {nullptr, nullptr};
-    if (LABELS) {
-        lab[0] = A.lab0 + off;
-        lab[1] = A.lab1 + off;
-    }
+    using CellT = Cell<T, LABELS>;
+    CellT* cells[2] = {static_cast<CellT*>(A.cell0) + off, static_cast<CellT*>(A.cell1) + off};
     int* level = A.level + off;
     int* pv = A.queue + off;
     int* limits = A.limits + off;
@@ -732,12 +785,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         if (A.phase_init) {
             // reset (ptp.cpp:61-68)
             for (int v = gtid; v < n; v += gthreads) {
-                dist[0][v] = inf;
-                dist[1][v] = inf;
-                if (LABELS) {
-                    lab[0][v] = -1;
-                    lab[1][v] = -1;
-                }
+                const CellT c = make_cell<T, LABELS>(inf, -1, 0);
+                st_cell(cells[0] + v, c);
+                st_cell(cells[1] + v, c);
                 if (A.fused_bfs) {
                     level[v] = -1;
                     pv[v] = -1;  // position not yet assigned (claim_records)
@@ -753,12 +803,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             // seed sources: d = 0, label = index in caller order (ptp.cpp:69-73)
             for (int s = gtid; s < m; s += gthreads) {
                 const int v = src[s];
-                dist[0][v] = T(0);
-                dist[1][v] = T(0);
-                if (LABELS) {
-                    lab[0][v] = s;
-                    lab[1][v] = s;
-                }
+                const CellT c = make_cell<T, LABELS>(T(0), s, 0);
+                st_cell(cells[0] + v, c);
+                st_cell(cells[1] + v, c);
                 if (A.fused_bfs) {
                     level[v] = 0;
                     pv[s] = v;
@@ -909,10 +956,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             }
             const unsigned long long it0 = A.dbg != nullptr ? cyc() : 0ull;
             const int prv = S.parity, cur_b = prv ^ 1;
-            const T* dp = dist[prv];
-            T* dcur = dist[cur_b];
-            const int* lp = LABELS ? lab[prv] : nullptr;
-            int* lc = LABELS ? lab[cur_b] : nullptr;
+            const CellT* cp = cells[prv];
+            CellT* ccur = cells[cur_b];
             const int bb_ = S.bb, be_ = S.be, fe_ = S.fe, oe_ = S.oe;
             const bool expand = S.expand != 0;
             // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
@@ -955,7 +1000,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x)
                         : nullptr;
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
-                                  cached, pack, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
+                                  cached, pack, p, kk, pv, pring, pL, pquad, cp, ccur, fe_,
                                   expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
                                   cb, ib, (dbg && t == 0) ? dslot : nullptr,
                                   kd, it0);
@@ -968,8 +1013,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     const int fp = f0 + tf * nb;
                     const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
                     const int v = tg.x == fp ? tg.y : (ldcg(pv + fp) & kIdMask);
-                    dcur[v] = ldcg(dp + v);
-                    if (LABELS) lc[v] = ldcg(lp + v);
+                    st_cell(ccur + v, ld_cell(cp + v));
                 }
             }
             } else {
@@ -988,7 +1032,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x)
                         : nullptr;
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
-                                  cached, pack, p, kk, pv, pring, pL, pquad, dp, dcur, lp, lc, fe_,
+                                  cached, pack, p, kk, pv, pring, pL, pquad, cp, ccur, fe_,
                                   expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
                                   cb, ib, (dbg && t == 0) ? dslot : nullptr,
                                   kd, it0);
@@ -1001,8 +1045,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     const int fp = f0 + tf * nb;
                     const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
                     const int v = tg.x == fp ? tg.y : (ldcg(pv + fp) & kIdMask);
-                    dcur[v] = ldcg(dp + v);
-                    if (LABELS) lc[v] = ldcg(lp + v);
+                    st_cell(ccur + v, ld_cell(cp + v));
                 }
             }
             if (dbg) {
@@ -1040,8 +1083,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                             if (p - (t % kChunk) >= oe_) break;
                             if (p < oe_) {
                                 wide_pre(p, N, pv, pring, nx);
-                                relax_wide2<T, LABELS>(M, A, p, kk, nx, pL, pquad, dp, dcur, lp,
-                                                       lc, fe_, eps, nonconv, my_max, calls, degs);
+                                relax_wide2<T, LABELS>(M, A, p, kk, nx, pL, pquad, cp, ccur, fe_,
+                                                       eps, nonconv, my_max, calls, degs);
                             }
                         }
                     } else {
@@ -1053,8 +1096,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         p = pos(t);
                         if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
                         if (pc < oe_)
-                            relax_wide2<T, LABELS>(M, A, pc, kk, cw, pL, pquad, dp, dcur, lp, lc,
-                                                   fe_, eps, nonconv, my_max, calls, degs);
+                            relax_wide2<T, LABELS>(M, A, pc, kk, cw, pL, pquad, cp, ccur, fe_,
+                                                   eps, nonconv, my_max, calls, degs);
                     }
                     }
             }
@@ -1151,11 +1194,11 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         double vmax = -1.0;
         int vidx = INT_MAX;
         if (A.out_dist != nullptr || A.fps_mode || A.out_labels != nullptr) {
-            const T* df = dist[fin];
-            const int* lf = LABELS ? lab[fin] : nullptr;
+            const CellT* cf = cells[fin];
             const long long qo = static_cast<long long>(q) * n;
             for (int v = gtid; v < n; v += gthreads) {
-                const T x = ldcg(df + v);
+                const CellT cx = ld_cell(cf + v);
+                const T x = cx.d;
                 if (A.out_dist != nullptr) {
                     if (A.out_double)
                         static_cast<double*>(A.out_dist)[qo + v] = static_cast<double>(x);
@@ -1163,7 +1206,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         static_cast<float*>(A.out_dist)[qo + v] = static_cast<float>(x);
                 }
                 if (A.out_labels != nullptr)
-                    A.out_labels[qo + v] = LABELS ? ldcg(lf + v) : (x != inf ? 0 : -1);
+                    A.out_labels[qo + v] = cx.lab();
                 const double xd = static_cast<double>(x);
                 if (xd > vmax || (xd == vmax && v < vidx)) {
                     vmax = xd;
