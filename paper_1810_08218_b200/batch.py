@@ -58,15 +58,17 @@ def run_sharded(mesh, queries, precision="single", groups=0, epsilon=1e-3, dst=0
         stats = solve(mesh, [queries[q] for q in mine], local)
     if world == 1:
         return local[:nq], stats
-    gathered = [torch.empty_like(local) for _ in range(world)] if rank == dst else None
-    dist.gather(local, gathered, dst=dst)
+    # NCCL gathers device buffers over NVLink; gloo (CPU tests) needs host copies
+    send = local if dist.get_backend() == "nccl" else local.cpu()
+    gathered = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
+    dist.gather(send, gathered, dst=dst)
     if rank != dst:
         return None, stats
     out = torch.empty((nq, n), dtype=dtype, device=dev)
     for r in range(world):
         idx = shard(nq, world, r)
         if idx:
-            out[torch.as_tensor(idx, device=dev)] = gathered[r][:len(idx)]
+            out[torch.as_tensor(idx, device=dev)] = gathered[r][:len(idx)].to(dev)
     return out, stats
 
 

@@ -394,6 +394,9 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
 #define GEODIST_DYN_CHUNKS 1
 #endif
 constexpr bool kDynChunks = GEODIST_DYN_CHUNKS != 0;
+#ifndef GEODIST_THREAD_WIDE
+#define GEODIST_THREAD_WIDE 1
+#endif
 
 struct WidePre {
     int vr;
@@ -977,7 +980,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
             // (the wide-only instantiation has no narrow path to protect: fp64 too, but
             // not fp64 with labels, whose per-thread fan spills)
-            constexpr bool kThreadWide = sizeof(T) == 4 || MODE == 2;
+            constexpr bool kThreadWide = GEODIST_THREAD_WIDE && (sizeof(T) == 4 || MODE == 2);
             // Wide iterations (fp32): positions are dealt to CTAs in chunks of 32
             // consecutive positions (chunk c -> CTA c mod nb) instead of one by one, so
             // a warp works on 32 neighbouring positions: their records are adjacent and,

@@ -65,3 +65,45 @@ def test_shard_partition():
             assert sorted(sum(parts, [])) == list(range(nq))
             assert max(map(len, parts)) - min(map(len, parts)) <= 1
     assert batch.even_sources(1000, 4) == [[0], [250], [500], [750]]
+
+
+def gpu_worker(rank, world, port, ret):
+    """One rank of the real sharded batch: the B200 solver on cuda:0 (both ranks share
+    the device), gloo for the gather (the BENCH_FORCE_DEVICE / BENCH_DIST_BACKEND=gloo
+    configuration of bench.py)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import paper_1810_08218_b200 as g
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    v, f = g.noisy_icosphere_arrays(5, 2e-3, 1)
+    M = g.Mesh(v, f, device=0)
+    queries = batch.even_sources(len(v), 7)
+    fields, stats = batch.run_sharded(M, queries, precision="single", groups=2)
+    assert len(stats) == len(batch.shard(len(queries), world, rank))
+    if rank == 0:
+        ret.put(fields.cpu().numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_real_solver_world2():
+    """world_size 2 over gloo with the real GPU solve on one device: the gathered fields
+    equal single-query runs bit for bit."""
+    import paper_1810_08218_b200 as g
+    world = 2
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=gpu_worker, args=(r, world, port, ret)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = ret.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    v, f = g.noisy_icosphere_arrays(5, 2e-3, 1)
+    M = g.Mesh(v, f)
+    for q, src in enumerate(batch.even_sources(len(v), 7)):
+        one = g.geodesics(M, src, precision="single")
+        assert np.array_equal(got[q].astype(np.float64).view(np.int64),
+                              one["distances"].view(np.int64)), q
