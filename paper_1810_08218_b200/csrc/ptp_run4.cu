@@ -39,6 +39,13 @@ constexpr int kLimRing = 1024;  // topleset limits kept on chip (levels)
 // n * 192 B through the L2 and evict the distance and level arrays.
 constexpr int kPacked = 1 << 30;
 
+struct T0State {
+    int k, i, rho, parity, bfs_open, done, tail, limk, bb, fe, frzb, frze, lim_top;
+    bool use_glim;
+    unsigned long long upd;
+    int sh_p0, sh_a0, sh_f0, sh_fa0, sh_nfz, pf, be_pub;
+};
+
 struct Bcast4 {
     int k, i, j, bb, oe, be, fe, frzb, frze, parity, done, expand;
     // this CTA's share (positions p == lb mod nb): band tasks p0 + t * nb below
@@ -609,6 +616,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
     constexpr int kB = run4_block(MODE);
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ Bcast4 S;
+    __shared__ T0State s_t0;
     __shared__ int s_lim[kLimRing];
     __shared__ int s_list[kSmemClaims];
     __shared__ T red_t[kB / 32];
@@ -714,11 +722,30 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         const int m = A.src_off ? A.src_off[q + 1] - s0 : A.src_count;
         const int* src = A.src + s0;
         // thread-0 loop state (identical in every CTA of the group)
-        int k = 0, i = 1, rho = INT_MAX, parity = 0, bfs_open = 0, done = 0;
-        int tail = 0, limk = 0, bb = 0, fe = 0, frzb = 0, frze = 0;
-        int lim_top = -1;      // highest topleset limit index held in s_lim
-        bool use_glim = false; // limits read from global memory (ring too short)
-        unsigned long long upd = 0;
+        // thread-0 loop state: only thread 0 touches it (barrier post / publish).  The
+        // wide-only and the fp64 labelled instantiations keep it in shared memory (as
+        // registers it is live in every thread: -5 % on the torus, and the fp64 labelled
+        // narrow path spilled); the others in registers (it sits on the narrow
+        // iteration's critical path: +3 % there from shared memory)
+        T0State t0_local;
+        T0State& t0 = [&]() -> T0State& {
+            if constexpr (MODE == 2 || (sizeof(T) == 8 && LABELS)) return s_t0;
+            else return t0_local;
+        }();
+        int &k = t0.k, &i = t0.i, &rho = t0.rho, &parity = t0.parity, &bfs_open = t0.bfs_open,
+            &done = t0.done;
+        int &tail = t0.tail, &limk = t0.limk, &bb = t0.bb, &fe = t0.fe, &frzb = t0.frzb,
+            &frze = t0.frze;
+        int& lim_top = t0.lim_top;    // highest topleset limit index held in s_lim
+        bool& use_glim = t0.use_glim; // limits read from global memory (ring too short)
+        unsigned long long& upd = t0.upd;
+        if (tid == 0) {
+            k = 0; i = 1; rho = INT_MAX; parity = 0; bfs_open = 0; done = 0;
+            tail = 0; limk = 0; bb = 0; fe = 0; frzb = 0; frze = 0;
+            lim_top = -1;
+            use_glim = false;
+            upd = 0;
+        }
         auto lim = [&](int r) -> int {
             return (use_glim || r <= lim_top - kLimRing) ? ldcg(limits + r) : s_lim[r % kLimRing];
         };
@@ -742,14 +769,19 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             slot = qx + (lb >= r ? 0 : 1);
         };
         auto owned_count = [&](int first, int y) { return y > first ? div_nb(y - first + nb - 1) : 0; };
-        int sh_p0 = 0, sh_a0 = 0, sh_f0 = 0, sh_fa0 = 0, sh_nfz = 0;
+        int &sh_p0 = t0.sh_p0, &sh_a0 = t0.sh_a0, &sh_f0 = t0.sh_f0, &sh_fa0 = t0.sh_fa0,
+            &sh_nfz = t0.sh_nfz;
         auto shares_now = [&] {
             first_owned(bb, sh_p0, sh_a0);
             first_owned(frzb, sh_f0, sh_fa0);
             sh_nfz = owned_count(sh_f0, frze);
         };
-        int pf = -1;
-        int be_pub = 0;  // the band end publish() wrote to S.be (thread 0's copy)
+        int& pf = t0.pf;
+        int& be_pub = t0.be_pub;  // the band end publish() wrote to S.be (thread 0's copy)
+        if (tid == 0) {
+            pf = -1;
+            be_pub = 0;
+        }
         const bool tr0 = A.trace != nullptr && lb == 0;
         auto publish = [&] {
             S.done = done;
@@ -950,9 +982,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 }
             }
             const int kk = S.k;
-            const bool dbg = A.dbg != nullptr && tid == 0 && iters < A.dbg_iters;
+            const bool dbg = A.dbg != nullptr && tid == 0 && S.k - 1 < A.dbg_iters;
             unsigned long long* dslot =
-                dbg ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x) : nullptr;
+                dbg ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x) : nullptr;
             if (dbg) {
                 dslot[0] = gtimer();
                 dslot[18] = 0;
@@ -998,9 +1030,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
                 unsigned long long* kd =
-                    (A.dbg != nullptr && iters < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
+                    (A.dbg != nullptr && S.k - 1 < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
                      (tid & (kGroup - 1)) == 0)
-                        ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x)
+                        ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
                                   cached, pack, p, kk, pv, pring, pL, pquad, cp, ccur, fe_,
@@ -1030,9 +1062,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
                 unsigned long long* kd =
-                    (A.dbg != nullptr && iters < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
+                    (A.dbg != nullptr && S.k - 1 < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
                      (tid & (kGroup - 1)) == 0)
-                        ? A.dbg + kDbgSlots * (static_cast<size_t>(iters) * gridDim.x + blockIdx.x)
+                        ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
                                   cached, pack, p, kk, pv, pring, pL, pquad, cp, ccur, fe_,
