@@ -824,7 +824,8 @@ int geodist_toplesets(geodist_mesh_t mesh, const int32_t* sources, int32_t m, in
         if (!mh->t_sorted) {
             mh->t_sorted = dalloc<int>(n);
             mh->t_position = dalloc<int>(n);
-            mh->t_scratch_words = 2 * (static_cast<size_t>(n + 31) / 32 + 1);
+            // the (level, chunk) count table of the exact-order pass (toplesets.cu)
+            mh->t_scratch_words = std::max<size_t>(static_cast<size_t>(n) / 16 + 1, 1u << 22);
             mh->t_scratch = dalloc<int>(mh->t_scratch_words);
         }
         int* d_src = mh->upload_sources(s.data(), s.size());

@@ -4,11 +4,10 @@
 //                       reference src/toplesets.cpp:37-55): one group barrier per
 //                       level, warp-aggregated queue appends; levels come out
 //                       grouped (limits exact) but unordered inside a level
-//   sort_small_kernel   per level, ascending vertex id (toplesets.cpp:53) by an
-//                       in-shared-memory bitonic sort (levels <= kSortCap)
-//   rank_large_kernel   levels > kSortCap: bitmap of the level + word prefix
-//                       popcounts give every vertex its rank among smaller ids
-//   position_kernel     position[sorted[p]] = p (toplesets.cpp:38-41)
+//   level_count/scan/scatter_kernel  ascending vertex id inside every level
+//                       (toplesets.cpp:53) and position[sorted[p]] = p
+//                       (toplesets.cpp:38-41): a stable counting sort of the vertices
+//                       by level over chunks of consecutive ids, all levels at once
 //   reorder kernels     reorder_for_bands (toplesets.cpp:60-89): old_of_new =
 //                       sorted ++ unreachable in id order, inverse, face rewrite.
 //                       The permuted connectivity is a relabelling of the
@@ -22,8 +21,6 @@
 namespace gdb {
 
 constexpr int kTopoBlock = 512;
-constexpr int kSortCap = 8192;   // ints sorted in shared memory per level
-constexpr int kSortBlock = 1024;
 
 template <typename Post>
 __device__ __forceinline__ void topo_barrier(unsigned* bar, unsigned& epoch, unsigned nblk,
@@ -116,84 +113,74 @@ __global__ void __launch_bounds__(kTopoBlock) bfs_kernel(TopoArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(kSortBlock) sort_small_kernel(const int* queue,
-                                                                 const int* limits, int rho,
-                                                                 int* sorted) {
-    __shared__ int buf[kSortCap];
-    for (int r = blockIdx.x; r < rho; r += gridDim.x) {
-        const int lo = limits[r], sz = limits[r + 1] - lo;
-        if (sz > kSortCap) continue;
-        if (sz == 1) {
-            if (threadIdx.x == 0) sorted[lo] = queue[lo];
-            continue;
+// Exact order inside every level (ascending vertex id, toplesets.cpp:53) for all
+// levels at once, as a stable counting sort of the vertices by level over chunks of
+// consecutive ids: one warp per chunk counts its vertices per level, every level's
+// row of chunk counts is scanned into global offsets (limits[r] + earlier chunks),
+// and the warp scatters its chunk in id order.  position[v] comes out of the same pass.
+__global__ void level_count_kernel(const int* level, int n, int chunk, int nchunks,
+                                   int* cnt) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int c = w; c < nchunks; c += nw) {
+        const int v1 = min(n, (c + 1) * chunk);
+        for (int v0 = c * chunk; v0 < v1; v0 += 32) {
+            const int v = v0 + lane;
+            const int l = v < v1 ? level[v] : -1;
+            const unsigned peers = __match_any_sync(kFull, l);
+            if (l >= 0 && lane == __ffs(peers) - 1)
+                atomicAdd(cnt + static_cast<size_t>(l) * nchunks + c, __popc(peers));
         }
-        int P = 1;
-        while (P < sz) P <<= 1;
-        for (int x = threadIdx.x; x < P; x += kSortBlock) buf[x] = x < sz ? queue[lo + x] : INT_MAX;
-        __syncthreads();
-        for (int kk = 2; kk <= P; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int x = threadIdx.x; x < P; x += kSortBlock) {
-                    const int y = x ^ j;
-                    if (y > x) {
-                        const int u = buf[x], w = buf[y];
-                        const bool up = (x & kk) == 0;
-                        if ((u > w) == up) {
-                            buf[x] = w;
-                            buf[y] = u;
-                        }
-                    }
-                }
-                __syncthreads();
+    }
+}
+
+// one warp per level: exclusive scan of the level's chunk counts, offset by limits[r]
+__global__ void level_scan_kernel(const int* limits, int rho, int nchunks, int* cnt) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= rho) return;
+    int* row = cnt + static_cast<size_t>(r) * nchunks;
+    int run = limits[r];
+    for (int c0 = 0; c0 < nchunks; c0 += 32) {
+        const int c = c0 + lane;
+        const int x = c < nchunks ? row[c] : 0;
+        int incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (c < nchunks) row[c] = run + incl - x;
+        run += __shfl_sync(kFull, incl, 31);
+    }
+}
+
+__global__ void level_scatter_kernel(const int* level, int n, int chunk, int nchunks,
+                                     int* off, int* sorted, int* position) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int c = w; c < nchunks; c += nw) {
+        const int v1 = min(n, (c + 1) * chunk);
+        for (int v0 = c * chunk; v0 < v1; v0 += 32) {
+            const int v = v0 + lane;
+            const int l = v < v1 ? level[v] : -1;
+            const unsigned peers = __match_any_sync(kFull, l);
+            const int leader = __ffs(peers) - 1;
+            int* slot = off + static_cast<size_t>(l < 0 ? 0 : l) * nchunks + c;
+            int base = 0;
+            if (l >= 0 && lane == leader) base = *slot;
+            base = __shfl_sync(kFull, base, leader);
+            if (l >= 0) {
+                const int at = base + __popc(peers & ((1u << lane) - 1u));
+                sorted[at] = v;
+                position[v] = at;
+                if (lane == leader) *slot = base + __popc(peers);
             }
+            __syncwarp();  // the next step's leader reads the updated offsets
         }
-        for (int x = threadIdx.x; x < sz; x += kSortBlock) sorted[lo + x] = buf[x];
-        __syncthreads();
     }
-}
-
-// One CTA ranks one large level through a bitmap over vertex ids.
-__global__ void __launch_bounds__(1024) rank_large_kernel(const int* queue, int lo, int sz, int n,
-                                                          unsigned* bitmap, int* wprefix,
-                                                          int* sorted) {
-    __shared__ int part[1024];
-    const int words = (n + 31) / 32;
-    for (int x = threadIdx.x; x < sz; x += blockDim.x) {
-        const int v = queue[lo + x];
-        atomicOr(&bitmap[v >> 5], 1u << (v & 31));
-    }
-    __syncthreads();
-    const int per = (words + blockDim.x - 1) / blockDim.x;
-    const int w0 = threadIdx.x * per, w1 = min(words, w0 + per);
-    int cnt = 0;
-    for (int w = w0; w < w1; ++w) cnt += __popc(bitmap[w]);
-    part[threadIdx.x] = cnt;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan
-        const int add = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
-        __syncthreads();
-        part[threadIdx.x] += add;
-        __syncthreads();
-    }
-    int run = part[threadIdx.x] - cnt;
-    for (int w = w0; w < w1; ++w) {
-        wprefix[w] = run;
-        run += __popc(bitmap[w]);
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < sz; x += blockDim.x) {
-        const int v = queue[lo + x];
-        const int w = v >> 5;
-        const int rank = wprefix[w] + __popc(bitmap[w] & ((1u << (v & 31)) - 1u));
-        sorted[lo + rank] = v;
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < sz; x += blockDim.x) bitmap[queue[lo + x] >> 5] = 0u;
-}
-
-__global__ void position_kernel(const int* sorted, int reachable, int* position) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < reachable; p += gridDim.x * blockDim.x)
-        position[sorted[p]] = p;
 }
 
 int topo_max_blocks(int device) {
@@ -203,16 +190,15 @@ int topo_max_blocks(int device) {
     return per_sm * sms;
 }
 
-// scratch: >= 2 * ((n + 31) / 32 + 1) words.  Leaves sorted / limits /
-// position on the device and the number of levels in *rho_host.
+// scratch: the (level, chunk) count table, at least n / 1024 + 1 words (more words
+// allow smaller chunks).  Leaves sorted / limits / position on the device and the
+// number of levels in *rho_host.
 cudaError_t launch_toplesets(const TopoArgs& a, int* scratch, size_t scratch_words, int* rho_host,
                              cudaStream_t st) {
-    const int words = (a.n + 31) / 32 + 1;
-    if (scratch_words < static_cast<size_t>(2 * words)) return cudaErrorInvalidValue;
-    unsigned* bitmap = reinterpret_cast<unsigned*>(scratch);
-    int* wprefix = scratch + words;
+    int* counts = scratch;
+    const long long count_words = static_cast<long long>(scratch_words);
+    if (count_words < a.n / 1024 + 1) return cudaErrorInvalidValue;
     cudaError_t e = cudaMemsetAsync(&a.ctl->bar, 0, sizeof(unsigned), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * words, st);
     if (e != cudaSuccess) return e;
     TopoArgs args = a;
     void* params[] = {&args};
@@ -228,21 +214,23 @@ cudaError_t launch_toplesets(const TopoArgs& a, int* scratch, size_t scratch_wor
     e = cudaMemcpyAsync(lim.data(), a.limits, sizeof(int) * (rho + 1), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
-    const int grid = rho < 4 * 148 ? rho : 4 * 148;
-    sort_small_kernel<<<grid, kSortBlock, 0, st>>>(a.queue, a.limits, rho, a.sorted);
-    note_launch();
-    for (int r = 0; r < rho; ++r) {
-        const int sz = lim[r + 1] - lim[r];
-        if (sz > kSortCap) {
-            rank_large_kernel<<<1, 1024, 0, st>>>(a.queue, lim[r], sz, a.n, bitmap, wprefix,
-                                                  a.sorted);
-            note_launch();
-        }
-    }
     const int reach = lim[rho];
     if (reach > 0) {
-        position_kernel<<<(reach + 255) / 256 < 1184 ? (reach + 255) / 256 : 1184, 256, 0, st>>>(
-            a.sorted, reach, a.position);
+        // chunks of consecutive ids; the per-(level, chunk) table stays within the
+        // scratch the caller provides (count_words)
+        long long chunk = 1024;
+        while (static_cast<long long>(rho) * ((a.n + chunk - 1) / chunk) > count_words) chunk *= 2;
+        const int nchunks = static_cast<int>((a.n + chunk - 1) / chunk);
+        e = cudaMemsetAsync(counts, 0, sizeof(int) * static_cast<size_t>(rho) * nchunks, st);
+        if (e != cudaSuccess) return e;
+        const int wblocks = (nchunks + 7) / 8;  // 8 warps per block, one warp per chunk
+        level_count_kernel<<<wblocks, 256, 0, st>>>(a.level, a.n, static_cast<int>(chunk), nchunks,
+                                                   counts);
+        note_launch();
+        level_scan_kernel<<<(rho + 7) / 8, 256, 0, st>>>(a.limits, rho, nchunks, counts);
+        note_launch();
+        level_scatter_kernel<<<wblocks, 256, 0, st>>>(a.level, a.n, static_cast<int>(chunk),
+                                                     nchunks, counts, a.sorted, a.position);
         note_launch();
     }
     *rho_host = rho;
