@@ -108,6 +108,10 @@ struct Workspace {
     long long n = 0;
     void* cell0 = nullptr;  // Jacobi double buffer: Cell<T, LABELS> (<= 16 B) per vertex
     void* cell1 = nullptr;
+    void* pcell0 = nullptr;  // the same by BFS position (wide iterations)
+    void* pcell1 = nullptr;
+    int* posof = nullptr;
+    int* dflag = nullptr;    // wide-iteration relaxation marks, 2 per position
     int* level = nullptr;
     int* queue = nullptr;
     int* limits = nullptr;
@@ -134,6 +138,7 @@ struct Workspace {
         persisted_on = nullptr;
         for (void* p : {static_cast<void*>(limits), static_cast<void*>(ctl),
                         static_cast<void*>(scratch), static_cast<void*>(pring), pL, pquad,
+                        static_cast<void*>(dflag),
                         static_cast<void*>(blists)})
             if (p) cudaFree(p);
         const int keep = claim_min;
@@ -156,12 +161,15 @@ struct Workspace {
         {
             auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
             const size_t bc = up(e * kCellMaxBytes), b4 = up(e * sizeof(int));
-            hot_bytes = 2 * bc + 2 * b4;
+            hot_bytes = 4 * bc + 3 * b4;
             hot = dalloc<char>(hot_bytes);
             char* x = hot;
             cell0 = x; x += bc;
             cell1 = x; x += bc;
+            pcell0 = x; x += bc;
+            pcell1 = x; x += bc;
             level = reinterpret_cast<int*>(x); x += b4;
+            posof = reinterpret_cast<int*>(x); x += b4;
             queue = reinterpret_cast<int*>(x);
         }
         limits = dalloc<int>(static_cast<size_t>(g) * (nn + 2));
@@ -170,6 +178,7 @@ struct Workspace {
         scratch_blocks = blocks;
         scratch = dalloc<unsigned long long>(2 * static_cast<size_t>(blocks));
         pring = dalloc<int>(e * kEllW);
+        dflag = dalloc<int>(2 * e);
         pL = dalloc<double>(e * kEllW);
         pquad = dalloc<char>(e * kEllW * 4 * sizeof(double));
         // a CTA rarely claims more than a few times its share of a level; beyond the
@@ -212,6 +221,10 @@ struct Workspace {
         a.wide_factor = w ? atoi(w) : kWideFactor;
         a.cell0 = cell0;
         a.cell1 = cell1;
+        a.pcell0 = pcell0;
+        a.pcell1 = pcell1;
+        a.posof = posof;
+        a.dflag = dflag;
         a.level = level;
         a.queue = queue;
         a.limits = limits;
@@ -419,6 +432,14 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
                               std::min(run_max_blocks(prec, labels, mh->device, 1),
                                        run_max_blocks(prec, labels, mh->device, 2)));
     if (maxb <= 0) throw Fail(GEODIST_ECUDA, "run kernel cannot be resident on this device");
+    // With an IterationObserver the claim lists are sized for the worst case up front: a
+    // claim-list overflow redoes the field, and the observer must see every iteration
+    // exactly once (ptp.cpp:118-120).
+    if (q.observer != nullptr && q.cfg->precision == GEODIST_DOUBLE &&
+        mh->ws.claim_min < n + 1) {
+        mh->ws.release();
+        mh->ws.claim_min = n + 1;
+    }
     mh->ws.ensure(1, n, maxb);
     Workspace& ws = mh->ws;
     cudaStream_t st = mh->stream;
@@ -502,6 +523,10 @@ void run_solve(geodist_mesh_s* mh, const Solve& q) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, mh->ev0, mh->ev1);
         total_ms += ms;
+        static const bool log_launches = getenv("GEODIST_LAUNCH_LOG") != nullptr;
+        if (log_launches)
+            fprintf(stderr, "launch %d mode %d: %.3f ms, k %d, i %d, exit %d, done %d\n", launch,
+                    mode, ms, hctl.k, hctl.i, hctl.mode_exit, hctl.done);
         if (hctl.err >= 2) {
             // a CTA's claim list overflowed (the kernel stopped the field): redo it
             // with lists that cannot overflow, before any observer call sees it
@@ -990,9 +1015,12 @@ int geodist_ptp_ordered(geodist_mesh_t mesh, const int32_t* sources, int32_t m,
             if (s < 0 || s >= mh->n || position[s] == -1 || position[s] >= limits[1])
                 throw std::invalid_argument("ptp_run: ordering does not match the source set");
         }
-        for (int p = 0; p < reachable; ++p)
-            if (sorted[p] < 0 || sorted[p] >= mh->n)
+        // a vertex at two positions would have two cells in the position-indexed layout
+        std::vector<unsigned char> seen(static_cast<size_t>(mh->n), 0);
+        for (int p = 0; p < reachable; ++p) {
+            if (sorted[p] < 0 || sorted[p] >= mh->n || seen[sorted[p]]++)
                 throw std::invalid_argument("ptp_run: ordering built for a different mesh");
+        }
         cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
         Solve q;
         q.sources = sources;

@@ -15,7 +15,9 @@
 //                        Cell<T, LABELS> = distance (+ nearest-source label for
 //                        multi-source runs) + change stamp (ptp_common.cuh)
 //   level[n]             BFS level (-1 = unvisited), fused topleset discovery
+//   pcell0/pcell1[n]     the double buffer indexed by BFS position (wide iterations)
 //   queue[n]             vertices in BFS order, level r at [limits[r], limits[r+1])
+//   posof[n]             inverse of queue (-1: vertex not yet positioned)
 //   limits[n+2]
 #pragma once
 
@@ -97,6 +99,10 @@ struct RunArgs {
     // per-group buffers: group g at base + g * stride (elements)
     void* cell0;         // Cell<T, LABELS>[stride] per group
     void* cell1;
+    void* pcell0;        // the same cells indexed by BFS position (wide iterations)
+    void* pcell1;
+    int* posof;          // BFS position of each vertex, -1 before it is positioned
+    int* dflag;          // 2 x stride per group: relaxation marks by position (parity k & 1)
     int* level;
     int* queue;
     int* limits;

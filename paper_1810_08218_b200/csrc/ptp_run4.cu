@@ -38,6 +38,26 @@ constexpr int kLimRing = 1024;  // topleset limits kept on chip (levels)
 // serve the wide path); writing them on every first relaxation would stream
 // n * 192 B through the L2 and evict the distance and level arrays.
 constexpr int kPacked = 1 << 30;
+// packed ring entry flag: still a vertex id, its position was not known when the
+// record was written (the topleset after the vertex's own, claimed in the same
+// iteration); resolved through posof at a later relaxation.  Bit 30 is free in every
+// entry of a packed record (entry 0's corner-count field is <= 7 there).
+constexpr int kUnres = 1 << 30;
+// pv[p] flag: the vertex has a degenerate corner (its degenerate_calls count depends on
+// which of its corners are finite, so the change-driven worklist never skips it)
+constexpr int kAlways = 1 << 29;
+#ifndef GEODIST_WORKLIST
+#define GEODIST_WORKLIST 1
+#endif
+// Position-layout wide iterations relax only positions marked by a change in the
+// previous iteration (see the older-band loop); 0: every band position every iteration.
+// fp64 only: measured on the 1000^2 torus, fp64 17.3 ms with it vs 18.7 without, fp32
+// 15.3 vs 14.6 -- the scan trip costs more than the skipped fp32 relaxations save.
+template <typename T> __host__ __device__ constexpr bool worklist_for() { return GEODIST_WORKLIST != 0 && sizeof(T) == 8; }
+
+// Mark position q for relaxation in the next iteration (mark value kk + 1 in the array
+// of the next iteration's parity).  Plain stores: every writer stores the same value.
+__device__ __forceinline__ void mark(int* dnext, int q, int kk) { dnext[q] = kk + 1; }
 
 struct T0State {
     int k, i, rho, parity, bfs_open, done, tail, limk, bb, fe, frzb, frze, lim_top;
@@ -48,6 +68,7 @@ struct T0State {
 
 struct Bcast4 {
     int k, i, j, bb, oe, be, fe, frzb, frze, parity, done, expand;
+    int tail;  // positions assigned so far
     // this CTA's share (positions p == lb mod nb): band tasks p0 + t * nb below
     // be (record-cache slot a0 + t), frozen positions f0 + t * nb for t < nfz
     int p0, a0, f0, fa0, nfz;
@@ -161,8 +182,10 @@ struct ClaimCtx {
 template <typename T, bool LABELS>
 __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
                                        int sl, bool act, bool is_new, bool cached, bool pack,
-                                       int p, int kk, const int* pv, const int* pring, const T* pL,
-                                       const char* pquad, const Cell<T, LABELS>* cp,
+                                       bool posm,
+                                       int p, int kk, const int* pv, const int* posof,
+                                       int* pring, T* pL, char* pquad, int* dnext,
+                                       const Cell<T, LABELS>* cp,
                                        Cell<T, LABELS>* cc, int fe, bool expand, int* level, T eps,
                                        const ClaimCtx& CC, int& nonconv, T& my_max,
                                        long long& calls, long long& degs, bool& ca_claim,
@@ -197,7 +220,6 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
         }
     }
     if (act && !hit) {
-        const size_t pb = static_cast<size_t>(p) * kEllW;
         if (is_new) {
             // the claimer's warp 0 writes pv[p] right after its barrier arrival
             v = ld_relaxed_i32(pv + p);
@@ -210,42 +232,15 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                 v = ld_relaxed_i32(pv + p);
             }
             if (kdbg) kdbg[11] = gtimer_after(v) - k0;
+        } else {
+            v = ldcg(pv + p) & kIdMask;  // record-cache miss (first narrow iteration of a launch)
         }
-        bool packed = false;
-        if (!is_new) {
-            // packed record (if it was written) and the id, in one trip
-            const int vr = ldcg(pv + p);
-            // packed records are slot-major (slot s of position p at s * N + p)
-            const size_t N = static_cast<size_t>(A.stride);
-            const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
-            rr = make_int2(__ldcg(pring + s0), __ldcg(pring + s1));
-            La = ldcg(pL + s0);
-            Lb = ldcg(pL + s1);
-            qa.load_cg(pquad, s0);
-            qb.load_cg(pquad, s1);
-            packed = (vr & kPacked) != 0;
-            v = vr & kIdMask;
-        }
-        if (!packed) {
-            // first relaxation (or no packed record): the id-indexed ELL row (pulled
-            // into L2 by the claimer)
-            const size_t eb = static_cast<size_t>(v) * kEllW;
-            rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
-            Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
-            qa.load(M.equad, static_cast<int>(eb + 2 * gl));
-            qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
-            if (is_new && pack) {
-                const size_t N = static_cast<size_t>(A.stride);
-                const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
-                const_cast<int*>(pring)[s0] = rr.x;
-                const_cast<int*>(pring)[s1] = rr.y;
-                const_cast<T*>(pL)[s0] = La;
-                const_cast<T*>(pL)[s1] = Lb;
-                qa.store_at(const_cast<char*>(pquad), s0);
-                qb.store_at(const_cast<char*>(pquad), s1);
-                if (gl == 0) const_cast<int*>(pv)[p] = v | kPacked;
-            }
-        }
+        // the id-indexed ELL row (pulled into L2 by the claimer)
+        const size_t eb = static_cast<size_t>(v) * kEllW;
+        rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
+        Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
+        qa.load(M.equad, static_cast<int>(eb + 2 * gl));
+        qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
         if (cached) {
             C.pv[ci] = make_int2(p, v);
             C.rr[ci] = rr;
@@ -271,21 +266,58 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     int lv = -1, sv = 0;
     T ta = inf, tb = inf;
     int la = -1, lb_ = -1;
+    // cells: by vertex id in narrow iterations, by BFS position in wide ones (the
+    // neighbours' positions from posof; a neighbour without one yet is in the topleset
+    // being claimed now, never relaxed: +inf)
+    const int sidx = posm ? p : v;
+    int pa = ida, pb_ = idb;
+    if (posm) {
+        pa = hasa ? ldcg(posof + ida) : -1;
+        pb_ = hasb ? ldcg(posof + idb) : -1;
+    }
     if (act && gl == 0) {
-        const Cell<T, LABELS> c = ld_cell(cp + v);
+        const Cell<T, LABELS> c = ld_cell(cp + sidx);
         tv = c.d;
         lv = c.lab();
         sv = c.stamp();
     }
-    if (hasa) {
-        const Cell<T, LABELS> c = ld_cell(cp + ida);
+    if (hasa && pa >= 0) {
+        const Cell<T, LABELS> c = ld_cell(cp + pa);
         ta = c.d;
         la = c.lab();
     }
-    if (hasb) {
-        const Cell<T, LABELS> c = ld_cell(cp + idb);
+    if (hasb && pb_ >= 0) {
+        const Cell<T, LABELS> c = ld_cell(cp + pb_);
         tb = c.d;
         lb_ = c.lab();
+    }
+    // any degenerate corner of the vertex (bit 31 of the corner's first entry), for the
+    // packed record's kAlways flag (all lanes take part in the shuffles)
+    int dg = 0;
+    if (pack) {  // CTA-uniform
+        dg = ((gl < d && rr.x < 0) || (gl + kGroup < d && rr.y < 0)) ? 1 : 0;
+        dg |= __shfl_xor_sync(kFull, dg, 1, kGroup);
+        dg |= __shfl_xor_sync(kFull, dg, 2, kGroup);
+    }
+    if (pack && is_new && !ovf) {
+        // the packed record, written at the first relaxation from the ELL row the claimer
+        // pulled into L2: ring entries as positions (an entry without one yet keeps its id,
+        // flagged kUnres), |x|, quads; slots 2gl and 2gl+1 = entries gl and gl+4
+        const size_t N = static_cast<size_t>(A.stride);
+        const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
+        const int fa = rr.x & ~kIdMask, fb = rr.y & ~kIdMask;
+        if (posm) {
+            pring[s0] = !hasa ? rr.x : pa >= 0 ? (fa | pa) : (fa | kUnres | ida);
+            pring[s1] = !hasb ? rr.y : pb_ >= 0 ? (fb | pb_) : (fb | kUnres | idb);
+        } else {
+            pring[s0] = rr.x;
+            pring[s1] = rr.y;
+        }
+        pL[s0] = La;
+        pL[s1] = Lb;
+        qa.store_at(pquad, s0);
+        qb.store_at(pquad, s1);
+        if (gl == 0) const_cast<int*>(pv)[p] = v | kPacked | (dg ? kAlways : 0);
     }
     // BFS claims (toplesets.cpp:44-52), issued after the distance loads: an atomic
     // ahead of them in the memory pipeline would delay the loads
@@ -342,13 +374,15 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                 if (ha) cA = atomicCAS(level + ia, -1, kk + 1) == -1;
                 if (hb) cB = atomicCAS(level + ib, -1, kk + 1) == -1;
             }
-            if (ha) {
-                const Cell<T, LABELS> c = ld_cell(cp + ia);
+            const int pA = posm && ha ? ldcg(posof + ia) : ia;
+            const int pB = posm && hb ? ldcg(posof + ib) : ib;
+            if (ha && pA >= 0) {
+                const Cell<T, LABELS> c = ld_cell(cp + pA);
                 TA = c.d;
                 lA = c.lab();
             }
-            if (hb) {
-                const Cell<T, LABELS> c = ld_cell(cp + ib);
+            if (hb && pB >= 0) {
+                const Cell<T, LABELS> c = ld_cell(cp + pB);
                 TB = c.d;
                 lB = c.lab();
             }
@@ -371,10 +405,27 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
             if (LABELS) blab = ol;
         }
     }
+    if (posm && worklist_for<T>() && dnext != nullptr) {
+        // worklist marks: a changed vertex and its positioned neighbours are relaxed next
+        // iteration (neighbours without a position are the next newest topleset)
+        const bool chg = __shfl_sync(kFull, static_cast<int>(act && best != tv), g0) != 0;
+        if (chg) {
+            if (gl == 0) mark(dnext, p, kk);
+            if (hasa && pa >= 0) mark(dnext, pa, kk);
+            if (hasb && pb_ >= 0) mark(dnext, pb_, kk);
+            if (ovf && gl == 0) {
+                const int c0 = __ldg(M.cptr + v), r0 = c0 + v;
+                for (int e = 0; e <= d; ++e) {
+                    const int q = ldcg(posof + (__ldg(M.ring + r0 + e) & INT_MAX));
+                    if (q >= 0) mark(dnext, q, kk);
+                }
+            }
+        }
+    }
     if (act && gl == 0) {
         // the change stamp: this iteration if the distance changed (a label changes
         // only with its distance, update_kernel.hpp:114-117)
-        st_cell(cc + v, make_cell<T, LABELS>(best, blab, best != tv ? kk : sv));
+        st_cell(cc + sidx, make_cell<T, LABELS>(best, blab, best != tv ? kk : sv));
         calls += d;
         if (p < fe || A.last_change != nullptr) {
             const T rc = rel_change(tv, best);
@@ -390,20 +441,22 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
 // sequential strict-'<' fan scan of relax_vertex (update_kernel.hpp:93-120),
 // corners evaluated two at a time.
 // Wide relaxation, one vertex per thread, arranged for memory-level parallelism:
-// trip 1 loads the position's vertex id AND its packed ring ids (both addressed by the
-// position: slot s of p at s * N + p), trip 2 the neighbours' distances together with
-// |x| and the corner quads of the d live slots only, then the corners are evaluated.
-// (the first version's order -- vertex id, then ring ids, then distances -- was three
-// trips.)
-// A position without a packed record (entered the band while it was narrow) re-reads
-// its ring ids from the id-indexed ELL table: one more trip for those only.
+// trip 1 loads the position's vertex id AND its packed record's ring entries (both
+// addressed by the position: slot s of p at s * N + p), trip 2 the neighbours' cells
+// together with |x| and the corner quads of the d live slots only, then the corners are
+// evaluated.  Wide iterations keep the Jacobi cells indexed by BFS position (the
+// reorder_for_bands layout, toplesets.cpp:60-89): the packed ring entries are the
+// neighbours' POSITIONS, so a warp over 32 consecutive positions gathers from a few
+// runs of the adjacent toplesets instead of 32 x 7 scattered vertex ids, and its own
+// cell loads and stores are coalesced.
+// A position without a packed record (its first wide relaxation) reads its ring from
+// the id-indexed ELL table, maps the ids to positions (posof) and writes the record
+// once every neighbour has a position (the topleset after its own is positioned at the
+// barrier that ends its first relaxation, and that flush is visible one iteration later).
 #ifndef GEODIST_DYN_CHUNKS
 #define GEODIST_DYN_CHUNKS 1
 #endif
 constexpr bool kDynChunks = GEODIST_DYN_CHUNKS != 0;
-#ifndef GEODIST_THREAD_WIDE
-#define GEODIST_THREAD_WIDE 1
-#endif
 
 struct WidePre {
     int vr;
@@ -412,7 +465,7 @@ struct WidePre {
 
 // trip 1 of a wide position (issued one position ahead by the caller)
 __device__ __forceinline__ void wide_pre(int p, size_t N, const int* pv, const int* pring,
-                                             WidePre& w) {
+                                         WidePre& w) {
     w.vr = ldcg(pv + p);
 #pragma unroll
     for (int e = 0; e < kEllW; ++e) w.raw[e] = __ldcg(pring + ell_slot(e) * N + p);
@@ -433,9 +486,10 @@ __device__ __forceinline__ void wide_pre(int p, size_t N, const int* pv, const i
 // after the stamps (a third trip for those only: the 2048^2 height field's band does
 // not fit L2, and the skipped loads are DRAM traffic).  Single-source runs evaluate
 // every corner with |x| and quads loaded together with the distances.
-template <typename T, bool LABELS>
+template <typename T, bool LABELS, bool POS>
 __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, int p, int kk,
-                                            const WidePre& w, const T* pL, const char* pquad,
+                                            const WidePre& w, int* pv, int* pring, T* pL,
+                                            char* pquad, const int* posof, int* dnext,
                                             const Cell<T, LABELS>* cp, Cell<T, LABELS>* cc,
                                             int fe, T eps, int& nonconv, T& my_max,
                                             long long& calls, long long& degs) {
@@ -449,6 +503,7 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
     size_t pb = static_cast<size_t>(p), step = N;
     const T* lsrc = pL;
     const char* qsrc = pquad;
+    unsigned unk = 0;  // entries whose neighbour has no position yet (+inf cells)
     if (!(vr & kPacked)) {
         pb = static_cast<size_t>(v) * kEllW;
         step = 1;
@@ -456,30 +511,84 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
         qsrc = static_cast<const char*>(M.equad);
 #pragma unroll
         for (int e = 0; e < kEllW; ++e) raw[e] = __ldcg(M.ering + pb + ell_slot(e));
+        const int d0 = (raw[0] >> kMetaShift) & 15;
+        if (POS && d0 != kEllOverflow) {
+            int ps[kEllW];
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e) ps[e] = e <= d0 ? ldcg(posof + (raw[e] & kIdMask)) : 0;
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e) {
+                if (ps[e] < 0) unk |= 1u << e;
+                raw[e] = (raw[e] & ~kIdMask) | (ps[e] & kIdMask);
+            }
+            if (unk == 0) {
+                // the packed record: ring entries as positions (flags kept), |x|, quads
+#pragma unroll
+                for (int e = 0; e < kEllW; ++e) {
+                    const size_t dst = static_cast<size_t>(ell_slot(e)) * N + p;
+                    const size_t src = pb + ell_slot(e);
+                    pring[dst] = raw[e];
+                    pL[dst] = ldcg(lsrc + src);
+                    Quad<T> qq;
+                    qq.load_cg(qsrc, src);
+                    qq.store_at(pquad, dst);
+                }
+                bool dg = false;
+#pragma unroll
+                for (int c = 0; c < kEllW - 1; ++c) dg |= c < d0 && raw[c] < 0;
+                pv[p] = v | kPacked | (dg ? kAlways : 0);
+            }
+        }
+    } else if (POS) {
+        // entries left unresolved by the first relaxation: resolved once their vertex
+        // has a position (and written back), +inf cells until then
+        unsigned unr = 0;
+#pragma unroll
+        for (int e = 0; e < kEllW; ++e) unr |= static_cast<unsigned>((raw[e] >> 30) & 1) << e;
+        if (unr) {
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e) {
+                if (!((unr >> e) & 1u)) continue;
+                raw[e] &= ~kUnres;
+                const int ps = ldcg(posof + (raw[e] & kIdMask));
+                if (ps >= 0) {
+                    raw[e] = (raw[e] & ~kIdMask) | ps;
+                    pring[static_cast<size_t>(ell_slot(e)) * N + p] = raw[e];
+                } else {
+                    unk |= 1u << e;
+                }
+            }
+        }
     }
     constexpr bool kSkip = LABELS;
-    const Cell<T, LABELS> self = ld_cell(cp + v);
+    const int sidx = POS ? p : v;  // this vertex's cell
+    const Cell<T, LABELS> self = ld_cell(cp + sidx);
     const T tv = self.d;
     const int lv = self.lab();
     const int prevk = kk - 1;
     int d = (raw[0] >> kMetaShift) & 15;
     T best = tv;
     int blab = lv;
-    if (d == kEllOverflow) {
+    const bool ovfl = d == kEllOverflow;
+    if (ovfl) {
         // more than 7 corners: CSR tables, sequential fan walk, every corner evaluated
         const int c0 = __ldg(M.cptr + v);
         d = __ldg(M.cptr + v + 1) - c0;
         const int r0 = c0 + v;
         const T* ringL = static_cast<const T*>(M.ringL);
+        auto cell_of = [&](int id) {
+            const int q = POS ? ldcg(posof + id) : id;
+            return q >= 0 ? ld_cell(cp + q) : make_cell<T, LABELS>(inf, -1, 0);
+        };
         int x0 = __ldg(M.ring + r0);
         int i0 = x0 & INT_MAX;
-        Cell<T, LABELS> n0 = ld_cell(cp + i0);
+        Cell<T, LABELS> n0 = cell_of(i0);
         T t0 = n0.d, L0 = __ldg(ringL + r0);
         int l0 = n0.lab();
         for (int c = 0; c < d; ++c) {
             const int x1 = __ldg(M.ring + r0 + c + 1);
             const int i1 = x1 & INT_MAX;
-            const Cell<T, LABELS> n1 = ld_cell(cp + i1);
+            const Cell<T, LABELS> n1 = cell_of(i1);
             const T t1 = n1.d, L1 = __ldg(ringL + r0 + c + 1);
             const int l1 = n1.lab();
             Quad<T> q;
@@ -510,7 +619,8 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
             if (e < kEllW) L[e] = T(0);
             if (e < kQ) q[e].q11 = q[e].q12 = q[e].q22 = q[e].a = T(0);
             if (e < kEllW && e <= d) {
-                const Cell<T, LABELS> c = ld_cell(cp + (raw[e] & kIdMask));
+                const Cell<T, LABELS> c = (unk >> e) & 1u ? make_cell<T, LABELS>(inf, -1, 0)
+                                                          : ld_cell(cp + (raw[e] & kIdMask));
                 t[e] = c.d;
                 l[e] = c.lab();
                 ch[e] = !kSkip || c.stamp() == prevk;
@@ -593,10 +703,25 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
         }
     }
     calls += d;
+    if (POS && worklist_for<T>() && best != tv) {
+        // worklist marks for the next iteration: this vertex and its positioned neighbours
+        mark(dnext, p, kk);
+        if (ovfl) {
+            const int r0 = __ldg(M.cptr + v) + v;
+            for (int e = 0; e <= d; ++e) {
+                const int q = ldcg(posof + (__ldg(M.ring + r0 + e) & INT_MAX));
+                if (q >= 0) mark(dnext, q, kk);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e)
+                if (e <= d && !((unk >> e) & 1u)) mark(dnext, raw[e] & kIdMask, kk);
+        }
+    }
     // The other buffer holds this vertex's cell of two iterations ago: rewrite it only
     // if the value changed now or last iteration.
     if (!kSkip || best != tv || self.stamp() == prevk)
-        st_cell(cc + v, make_cell<T, LABELS>(best, blab, best != tv ? kk : self.stamp()));
+        st_cell(cc + sidx, make_cell<T, LABELS>(best, blab, best != tv ? kk : self.stamp()));
     if (best != tv && (p < fe || A.last_change != nullptr)) {
         const T rc = rel_change(tv, best);
         if (p < fe && rc >= eps) nonconv = 1;
@@ -625,7 +750,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
     __shared__ int red_i[kB / 32];
     __shared__ int s_ccnt, s_err;
     __shared__ int s_chunk;  // next older-band chunk of this CTA (wide iterations)
-    __shared__ unsigned long long s_bw;
+    __shared__ int s_qn, s_qh;  // worklist length / next batch (wide iterations)
 
     const int tid = threadIdx.x;
     constexpr int R = kCacheSlots;
@@ -639,8 +764,12 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
     const long long off8 = off * kEllW;
     using CellT = Cell<T, LABELS>;
     CellT* cells[2] = {static_cast<CellT*>(A.cell0) + off, static_cast<CellT*>(A.cell1) + off};
+    // the same double buffer indexed by BFS position (wide iterations)
+    CellT* pcells[2] = {static_cast<CellT*>(A.pcell0) + off, static_cast<CellT*>(A.pcell1) + off};
     int* level = A.level + off;
     int* pv = A.queue + off;
+    int* posof = A.posof + off;  // BFS position of a vertex (-1: not yet positioned)
+    int* dflag = A.dflag + 2 * off;  // worklist marks by position, [parity][n]
     int* limits = A.limits + off;
     int* pring = A.pring + off8;
     T* pL = static_cast<T*>(A.pL) + off8;
@@ -684,10 +813,14 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 // abandoned at this barrier and redone with larger lists); their
                 // positions get vertex 0, an in-bounds placeholder
                 const int at = level_start + static_cast<int>(__shfl_sync(kFull, old, 0) >> 32);
-                for (int x = tid; x < cnt; x += 32)
-                    pv[at + x] = x < kSmemClaims           ? s_list[x]
-                                 : x - kSmemClaims < A.claim_cap ? g_list[x - kSmemClaims]
-                                                                 : 0;
+                for (int x = tid; x < cnt; x += 32) {
+                    const bool kept = x < kSmemClaims || x - kSmemClaims < A.claim_cap;
+                    const int id = x < kSmemClaims ? s_list[x]
+                                   : kept          ? g_list[x - kSmemClaims]
+                                                   : 0;
+                    pv[at + x] = id;
+                    if (kept) posof[id] = at + x;
+                }
             }
             if (tid == 0) {
                 unsigned long long x = old + payload + 1ull;
@@ -785,8 +918,11 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         const bool tr0 = A.trace != nullptr && lb == 0;
         auto publish = [&] {
             S.done = done;
+            S.tail = tail;
             s_ccnt = 0;
             s_chunk = 0;
+            s_qn = 0;
+            s_qh = 0;
             if (done) return;
             const int kk = k + 1;
             const int j = bfs_open ? kk : min(kk, rho - 1);
@@ -827,6 +963,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     level[v] = -1;
                     pv[v] = -1;  // position not yet assigned (claim_records)
                 }
+                posof[v] = -1;
+                dflag[v] = 0;
+                dflag[n + v] = 0;
                 if (A.last_change) A.last_change[v] = 0;
             }
             if (gtid == 0) {
@@ -844,6 +983,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 if (A.fused_bfs) {
                     level[v] = 0;
                     pv[s] = v;
+                    posof[v] = s;
                 }
             }
             if (A.fused_bfs && gtid == 0) {
@@ -851,21 +991,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 limits[1] = m;
             }
             if (!A.fused_bfs) {
-                // caller ordering: pack every reachable position's record up front
+                // caller ordering: every reachable vertex's position up front
                 const int reach = ldcg(limits + A.given_rho);
-                for (long long x = gtid; x < static_cast<long long>(reach) * kEllW;
-                     x += gthreads) {
-                    const int p = static_cast<int>(x / kEllW), slot = static_cast<int>(x % kEllW);
-                    const int v = ldcg(pv + p) & kIdMask;
-                    const size_t eb = static_cast<size_t>(v) * kEllW + slot;
-                    const size_t dst = static_cast<size_t>(slot) * A.stride + p;  // slot-major
-                    pring[dst] = __ldg(M.ering + eb);
-                    pL[dst] = __ldg(static_cast<const T*>(M.eL) + eb);
-                    Quad<T> qq;
-                    qq.load(M.equad, static_cast<int>(eb));
-                    qq.store_at(pquad, dst);
-                    if (slot == 0) pv[p] = v | kPacked;
-                }
+                for (int p = gtid; p < reach; p += gthreads) posof[ldcg(pv + p) & kIdMask] = p;
             }
             if (tid == 0) s_ccnt = 0;
             barrier(0ull, 0, [] {}, [](unsigned long long) {});
@@ -964,6 +1092,37 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             __syncthreads();
         }
 
+        // Cell layout: narrow iterations index the double buffer by vertex id (the record
+        // cache holds ring ids), wide ones by BFS position (pcells; packed ring entries
+        // are positions).  Every launch starts and ends in the id layout; crossing over
+        // is one pass over the positions assigned so far, both buffers, and a barrier.
+        int layout = 0;
+        bool fresh = false;
+        constexpr bool kPosLayout = !LABELS;
+        auto relayout = [&](int to) {
+            const int top = S.tail;
+            const CellT none = make_cell<T, LABELS>(inf, -1, 0);
+            for (int x = gtid; x < n; x += gthreads) {
+                // a position flushed at the last barrier may not be visible yet (-1): its
+                // vertex has not been relaxed, +inf in both layouts
+                const int id = x < top ? ldcg(pv + x) : -1;
+                const int v = id & kIdMask;
+                if (to == 1) {
+                    st_cell(pcells[0] + x, id >= 0 ? ld_cell(cells[0] + v) : none);
+                    st_cell(pcells[1] + x, id >= 0 ? ld_cell(cells[1] + v) : none);
+                } else if (id >= 0) {
+                    st_cell(cells[0] + v, ld_cell(pcells[0] + x));
+                    st_cell(cells[1] + v, ld_cell(pcells[1] + x));
+                }
+            }
+            // wide iterations reuse the record cache's shared memory as the worklist queue
+            if (to == 0 && kPosLayout && worklist_for<T>())
+                for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
+            barrier(0ull, 0, [] {}, [](unsigned long long) {});
+            layout = to;
+            fresh = to == 1;  // no marks yet: the first wide iteration relaxes every position
+        };
+
         long long calls = 0, degs = 0;
         int iters = 0;
         int mode_exit = 0;
@@ -991,15 +1150,23 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             }
             const unsigned long long it0 = A.dbg != nullptr ? cyc() : 0ull;
             const int prv = S.parity, cur_b = prv ^ 1;
-            const CellT* cp = cells[prv];
-            CellT* ccur = cells[cur_b];
             const int bb_ = S.bb, be_ = S.be, fe_ = S.fe, oe_ = S.oe;
             const bool expand = S.expand != 0;
             // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
             const bool cached = MODE == 1   ? true
                                 : MODE == 2 ? false
                                             : A.wide_factor != 0 && (be_ - bb_) <= (kCacheSlots - 1) * nb;
-            const bool pack = !cached || 2 * (be_ - bb_) > (kCacheSlots - 1) * nb;
+            // single-source fields relax wide bands in the position layout; labelled ones
+            // keep the id layout (measured: the 2048^2 height field's band does not fit L2,
+            // and its row-major ids give each vertex's gathers shared sectors)
+            const bool posl = kPosLayout && !cached;
+            if ((posl ? 1 : 0) != layout) relayout(posl ? 1 : 0);
+            const CellT* cp = posl ? pcells[prv] : cells[prv];
+            CellT* ccur = posl ? pcells[cur_b] : cells[cur_b];
+            // id layout: records are packed (ring ids) from the first relaxation once the
+            // band approaches the record cache's capacity, ready for the wide path
+            const bool pack = !kPosLayout && 2 * (be_ - bb_) > (kCacheSlots - 1) * nb;
+            int* dnext = posl ? dflag + ((kk + 1) & 1) * n : nullptr;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
             const int p0 = S.p0, a0 = S.a0;
@@ -1007,12 +1174,6 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             int nonconv = 0;
             T my_max = T(0);
             constexpr int kGroups = kB / kGroup;
-            // wide iterations (band beyond the record cache, fp32): the generic loop takes
-            // only the newest topleset; older positions are relaxed one per thread below
-            // (fp64 keeps the 4-lane groups: the per-thread fan needs too many registers)
-            // (the wide-only instantiation has no narrow path to protect: fp64 too, but
-            // not fp64 with labels, whose per-thread fan spills)
-            constexpr bool kThreadWide = GEODIST_THREAD_WIDE && (sizeof(T) == 4 || MODE == 2);
             // Wide iterations (fp32): positions are dealt to CTAs in chunks of 32
             // consecutive positions (chunk c -> CTA c mod nb) instead of one by one, so
             // a warp works on 32 neighbouring positions: their records are adjacent and,
@@ -1035,7 +1196,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
                 relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
-                                  cached, pack, p, kk, pv, pring, pL, pquad, cp, ccur, fe_,
+                                  true, pack, false, p, kk, pv, posof, pring, pL, pquad, nullptr, cp,
+                                  ccur, fe_,
                                   expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
                                   cb, ib, (dbg && t == 0) ? dslot : nullptr,
                                   kd, it0);
@@ -1052,10 +1214,81 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 }
             }
             } else {
+            // worklist queue in the record cache's memory, structure of arrays: position,
+            // position word, the 8 packed ring entries (40 B per queued position)
+            constexpr int kQEnt = 10 * sizeof(int);
+            const int qcap = static_cast<int>(R * Cache<T>::bytes_per_slot() / kQEnt);
+            int* wq_p = reinterpret_cast<int*>(dsm);
+            int* wq_v = wq_p + qcap;
+            int* wq_r = wq_v + qcap;  // entry e of queued position x at wq_r[e * qcap + x]
+            // this CTA's older positions: chunks lb, lb + nb, ... of 32 from bb up to oe
+            const int span0 = oe_ - bb_ - lb * kChunk;
+            const int nch = span0 > 0 ? (span0 + nb * kChunk - 1) / (nb * kChunk) : 0;
+            const int total = nch * kChunk;
+            // (a CTA share beyond the queue's capacity relaxes every position this iteration)
+            const bool wl = kPosLayout && worklist_for<T>() && total <= qcap;
+            if (wl) {
+                // Change-driven worklist (position layout).  relax_vertex is a pure function
+                // of the neighbours' previous values and starts from the vertex's own previous
+                // value, which is <= every candidate it already evaluated: a position none of
+                // whose neighbours (nor itself) changed in the previous iteration would
+                // recompute exactly its value, and both buffers already hold it (it was
+                // rewritten when it last changed, or relaxed unchanged).  Skipping it is
+                // bit-identical (update_kernel.hpp:93-120, ptp.cpp:96-110): its relative
+                // change is 0, its corners are still counted (relax_calls, from the record's
+                // corner count), and a vertex with a degenerate corner is never skipped
+                // (kAlways).  Changed vertices mark themselves and their neighbours (mark());
+                // the first wide iteration after a layout switch relaxes everything.
+                // The CTA scans all its older positions at once -- one trip: position word,
+                // mark and packed ring entries (trip 1 of the relaxation) -- and queues the
+                // marked ones with their ring entries in shared memory; relaxing a queued
+                // position is then one trip (neighbour cells, |x|, quads).
+                const int* dcur = dflag + (kk & 1) * n;
+                const int lane = tid & 31;
+                const unsigned lt = (1u << lane) - 1u;
+                const size_t N = static_cast<size_t>(A.stride);
+                constexpr int kU = 4;
+                for (int t0 = 0; t0 < total; t0 += kB * kU) {
+                    int vr[kU], df[kU], pp[kU], rw[kU][kEllW];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int t = t0 + u * kB + tid;
+                        pp[u] = bb_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
+                        vr[u] = df[u] = 0;
+#pragma unroll
+                        for (int e = 0; e < kEllW; ++e) rw[u][e] = 0;
+                        if (t < total && pp[u] < oe_) {
+                            vr[u] = ldcg(pv + pp[u]);
+                            df[u] = ldcg(dcur + pp[u]);
+#pragma unroll
+                            for (int e = 0; e < kEllW; ++e)
+                                rw[u][e] = __ldcg(pring + ell_slot(e) * N + pp[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int t = t0 + u * kB + tid;
+                        const bool in = t < total && pp[u] < oe_;
+                        const bool dirty = in && (fresh || !(vr[u] & kPacked) ||
+                                                  (vr[u] & kAlways) || df[u] == kk);
+                        if (in && !dirty) calls += (rw[u][0] >> kMetaShift) & 7;
+                        const unsigned bal = __ballot_sync(kFull, dirty);
+                        int at = 0;
+                        if (lane == 0 && bal) at = atomicAdd(&s_qn, __popc(bal));
+                        at = __shfl_sync(kFull, at, 0) + __popc(bal & lt);
+                        if (dirty) {
+                            wq_p[at] = pp[u];
+                            wq_v[at] = vr[u];
+#pragma unroll
+                            for (int e = 0; e < kEllW; ++e) wq_r[e * qcap + at] = rw[u][e];
+                        }
+                    }
+                }
+                __syncthreads();
+            }
             for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
                 // the newest topleset here, older ones one vertex per thread below (relax_wide2)
-                const int wbase = kThreadWide ? oe_ : bb_;
-                const int p = wbase + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
+                const int p = oe_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
                 const bool act = p < be_;
                 const bool frz = tf < nfz;
                 if (!__any_sync(kFull, act || frz)) break;
@@ -1066,11 +1299,10 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                      (tid & (kGroup - 1)) == 0)
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
-                relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
-                                  cached, pack, p, kk, pv, pring, pL, pquad, cp, ccur, fe_,
-                                  expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
-                                  cb, ib, (dbg && t == 0) ? dslot : nullptr,
-                                  kd, it0);
+                relax4<T, LABELS>(M, A, C, 0, act, act, false, true, kPosLayout, p, kk, pv, posof, pring, pL,
+                                  pquad, dnext, cp, ccur,
+                                  fe_, expand, level, eps, CC, nonconv, my_max, calls, degs, ca,
+                                  ia, cb, ib, (dbg && t == 0) ? dslot : nullptr, kd, it0);
                 if (expand)
                     claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
                                      CC.ccnt, CC.err);
@@ -1078,16 +1310,15 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 if (frz && (tid & (kGroup - 1)) == 0) {
                     // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
                     const int fp = f0 + tf * nb;
-                    const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
-                    const int v = tg.x == fp ? tg.y : (ldcg(pv + fp) & kIdMask);
-                    st_cell(ccur + v, ld_cell(cp + v));
+                    const int fv = kPosLayout ? fp : (ldcg(pv + fp) & kIdMask);
+                    st_cell(ccur + fv, ld_cell(cp + fv));
                 }
             }
             if (dbg) {
                 dslot[17] = gtimer();
                 dslot[18] = wchunk ? 1 : 0;
             }
-            if constexpr (kThreadWide) {
+            {
                 // older band positions [bb, oe): one vertex per thread, chunked.  Warps
                 // take this CTA's chunks from a shared counter, so the warps that held the
                 // newest topleset's tasks (BFS claims: the longest chain) take fewer.
@@ -1109,6 +1340,31 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     // this one's distances are gathered and its corners evaluated
                     // (not with labels: the second record in flight spills registers)
                     const size_t N = static_cast<size_t>(A.stride);
+                    if (wl) {
+                        // the worklist built by the scan above: batches of 32 queued positions,
+                        // one per thread, trip 1 of the next batch in flight during this one
+                        const int qn = s_qn;
+                        auto grabq = [&]() {
+                            int h = 0;
+                            if (lane == 0) h = atomicAdd(&s_qh, 32);
+                            return __shfl_sync(kFull, h, 0);
+                        };
+                        while (true) {
+                            const int h = grabq();
+                            if (h >= qn) break;
+                            if (h + lane < qn) {
+                                const int x = h + lane;
+                                WidePre w;
+                                w.vr = wq_v[x];
+#pragma unroll
+                                for (int e = 0; e < kEllW; ++e) w.raw[e] = wq_r[e * qcap + x];
+                                relax_wide2<T, LABELS, kPosLayout>(M, A, wq_p[x], kk, w, pv, pring,
+                                                                   pL, pquad, posof, dnext, cp,
+                                                                   ccur, fe_, eps, nonconv, my_max,
+                                                                   calls, degs);
+                            }
+                        }
+                    } else {
                     int t = kDynChunks ? grab() * kChunk + lane : tid;
                     int p = pos(t);
                     WidePre nx;
@@ -1118,8 +1374,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                             if (p - (t % kChunk) >= oe_) break;
                             if (p < oe_) {
                                 wide_pre(p, N, pv, pring, nx);
-                                relax_wide2<T, LABELS>(M, A, p, kk, nx, pL, pquad, cp, ccur, fe_,
-                                                       eps, nonconv, my_max, calls, degs);
+                                relax_wide2<T, LABELS, kPosLayout>(M, A, p, kk, nx, pv, pring, pL, pquad,
+                                                       posof, dnext, cp, ccur, fe_, eps, nonconv,
+                                                       my_max, calls, degs);
                             }
                         }
                     } else {
@@ -1131,13 +1388,16 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         p = pos(t);
                         if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
                         if (pc < oe_)
-                            relax_wide2<T, LABELS>(M, A, pc, kk, cw, pL, pquad, cp, ccur, fe_,
-                                                   eps, nonconv, my_max, calls, degs);
+                            relax_wide2<T, LABELS, kPosLayout>(M, A, pc, kk, cw, pv, pring, pL, pquad, posof,
+                                                   dnext, cp, ccur, fe_, eps, nonconv, my_max, calls,
+                                                   degs);
+                    }
                     }
                     }
             }
             }
             if (dbg) dslot[7] = cyc();
+            fresh = false;
             nonconv = __syncthreads_or(nonconv);
             if (A.trace != nullptr) {
                 const T bmax = block_max(my_max, red_t);
@@ -1202,6 +1462,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             ++iters;
         }
 
+        if (layout != 0) relayout(0);  // launches end in the id layout
         // per-query statistics
         const long long bc = block_sum(calls, red_l);
         const long long bd = block_sum(degs, red_l);
