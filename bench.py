@@ -434,6 +434,20 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if is_batch:
+            # the same queries one field at a time on the whole GPU (every 16th source,
+            # untimed by the step clock): what batching buys per query
+            sample = queries[::16]
+            scratch = torch.empty((1, n), dtype=tdtype, device="cuda")
+            one = [g.batch_geodesics_device(mesh, [q], scratch[0].data_ptr(),
+                                            precision=args.precision)[0] for q in sample]
+            per_one = 1e3 * sum(x["device_seconds"] for x in one) / len(one)
+            u_one = sum(x["vertex_updates"] for x in one) / len(one)
+            line["vs_single_fields"] = {
+                "batched_ms_per_query": ms_field, "one_at_a_time_ms_per_query": per_one,
+                "sample": f"{len(sample)} of the {len(queries)} sources (every 16th), one "
+                          "field per launch sequence on the whole GPU, device time",
+                "U_per_query_sample": u_one}
         if e2e_ms is not None:
             line["e2e"] = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 4,
                            "d2h_bytes_per_step": 8 * n,
