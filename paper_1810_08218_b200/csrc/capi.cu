@@ -102,6 +102,15 @@ void require_device(int device) {
 
 }  // namespace
 
+// fp32 multi-source cells pack the label into 24 bits (ptp_common.cuh Cell<float, true>)
+constexpr long long kMaxLabels32 = (1 << 24) - 2;
+static void check_label_range(int prec, long long m) {
+    if (prec == GEODIST_SINGLE && m > kMaxLabels32)
+        throw std::invalid_argument(
+            "ptp_run: single-precision multi-source fields support at most 16777214 sources "
+            "(use double precision)");
+}
+
 // Per-query device workspace for `groups` concurrent queries.
 struct Workspace {
     int groups = 0;
@@ -426,6 +435,7 @@ struct Solve {
 void run_solve(geodist_mesh_s* mh, const Solve& q) {
     const int prec = q.cfg->precision;
     const bool labels = q.m > 1;  // single source: labels are provably inert
+    check_label_range(prec, q.m);
     mh->ensure_prec(prec);
     const int n = mh->n;
     const int maxb = std::min(run_max_blocks(prec, labels, mh->device, 0),
@@ -1069,6 +1079,7 @@ int geodist_fps(geodist_mesh_t mesh, int32_t count, int32_t seed, const geodist_
         check_config(config);
         cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
         const int prec = config->precision;
+        check_label_range(prec, count);  // the last round labels all count samples
         mh->ensure_prec(prec);
     fps_retry:
         int maxb = INT_MAX;
@@ -1206,6 +1217,7 @@ int geodist_batch_device(geodist_mesh_t mesh, const int32_t* sources, const int3
         for (int q = 0; q < nq; ++q) {
             checked_sources(sources + offsets[q], offsets[q + 1] - offsets[q], mh->n);
             multi = multi || offsets[q + 1] - offsets[q] > 1;
+            check_label_range(config->precision, offsets[q + 1] - offsets[q]);
         }
         cuda_ok(cudaSetDevice(mh->device), "cudaSetDevice");
         const int prec = config->precision;

@@ -623,7 +623,7 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
                                                           : ld_cell(cp + (raw[e] & kIdMask));
                 t[e] = c.d;
                 l[e] = c.lab();
-                ch[e] = !kSkip || c.stamp() == prevk;
+                ch[e] = !kSkip || c.changed_at(prevk);
                 // fp64: |x| and the quads are loaded per corner pair below (registers)
                 if (!kSkip && sizeof(T) == 4) L[e] = ldcg(lsrc + pb + ell_slot(e) * step);
                 if (!kSkip && sizeof(T) == 4 && e < kQ && e < d)
@@ -720,7 +720,7 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
     }
     // The other buffer holds this vertex's cell of two iterations ago: rewrite it only
     // if the value changed now or last iteration.
-    if (!kSkip || best != tv || self.stamp() == prevk)
+    if (!kSkip || best != tv || self.changed_at(prevk))
         st_cell(cc + sidx, make_cell<T, LABELS>(best, blab, best != tv ? kk : self.stamp()));
     if (best != tv && (p < fe || A.last_change != nullptr)) {
         const T rc = rel_change(tv, best);
