@@ -63,12 +63,15 @@ struct T0State {
     int k, i, rho, parity, bfs_open, done, tail, limk, bb, fe, frzb, frze, lim_top;
     bool use_glim;
     unsigned long long upd;
-    int sh_p0, sh_a0, sh_f0, sh_fa0, sh_nfz, pf, be_pub;
+    int sh_p0, sh_a0, sh_f0, sh_fa0, sh_nfz, pf, be_pub, sh_x0, sh_xa0;
 };
 
 struct Bcast4 {
     int k, i, j, bb, oe, be, fe, frzb, frze, parity, done, expand;
     int tail;  // positions assigned so far
+    // BFS tasks (one topleset ahead of the band): positions [be, xe); this CTA's first one
+    // (xp0, cache slot xa0)
+    int xe, xp0, xa0;
     // this CTA's share (positions p == lb mod nb): band tasks p0 + t * nb below
     // be (record-cache slot a0 + t), frozen positions f0 + t * nb for t < nfz
     int p0, a0, f0, fa0, nfz;
@@ -432,6 +435,114 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
             if (p < fe && rc >= eps) nonconv = 1;
             if (p < fe && rc > my_max) my_max = rc;
             if (A.last_change != nullptr && rc >= eps) A.last_change[v] = kk;
+        }
+    }
+}
+
+// BFS one topleset ahead of the band (toplesets.cpp:37-55).  At iteration k the band's
+// newest topleset is level k, and a BFS task per position of level k + 1 (positioned at
+// the barrier that ended iteration k - 1) reads the vertex's ELL row -- into its record-
+// cache slot in narrow iterations, into its packed record in wide ones -- and claims its
+// unvisited neighbours for level k + 2 (atomicCAS on `level`; positions are assigned at
+// this iteration's barrier).  Level k + 1 is relaxed for the first time at iteration k + 1
+// from the row its BFS task left on chip: the relaxation's chain no longer carries the pv
+// and row trips nor the claims' atomics.  4-lane group per position, lanes return their
+// claims in (ca, ia, cb, ib).
+template <typename T>
+__device__ __forceinline__ void bfs4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
+                                     int sl, bool act, bool cached, bool pack, bool posm, int p,
+                                     int lvl,
+                                     int* pv, const int* posof, int* pring, T* pL, char* pquad,
+                                     int* level, const ClaimCtx& CC, bool& ca_claim, int& ida,
+                                     bool& cb_claim, int& idb) {
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int g0 = (threadIdx.x & 31) & ~(kGroup - 1);
+    int v = 0;
+    int2 rr = make_int2(0, 0);
+    T La = T(0), Lb = T(0);
+    Quad<T> qa, qb;
+    qa.q11 = qa.q12 = qa.q22 = qa.a = T(0);
+    qb = qa;
+    if (act) {
+        // the claimer's warp 0 wrote pv[p] right after its barrier arrival
+        v = ld_relaxed_i32(pv + p);
+        for (int spin = 0; v < 0; ++spin) {
+            if (spin > (1 << 22)) {
+                *CC.err = 3;
+                v = 0;
+                break;
+            }
+            v = ld_relaxed_i32(pv + p);
+        }
+        const size_t eb = static_cast<size_t>(v) * kEllW;
+        rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
+        Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
+        qa.load(M.equad, static_cast<int>(eb + 2 * gl));
+        qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
+    }
+    const int meta = __shfl_sync(kFull, rr.x, g0);
+    int d = act ? (meta >> kMetaShift) & 15 : 0;
+    const bool ovf = d == kEllOverflow;
+    ida = rr.x & kIdMask;
+    idb = rr.y & kIdMask;
+    const bool hasa = act && !ovf && d > 0 && gl <= d;
+    const bool hasb = act && !ovf && d > 0 && gl + kGroup <= d;
+    ca_claim = hasa && atomicCAS(level + ida, -1, lvl) == -1;
+    cb_claim = hasb && atomicCAS(level + idb, -1, lvl) == -1;
+    if (cached && act) {
+        const int ci = sl * 4 + gl;
+        C.pv[ci] = make_int2(p, v);
+        C.rr[ci] = rr;
+        C.L[2 * ci] = La;
+        C.L[2 * ci + 1] = Lb;
+        sm_store_quad<T>(C.q + 2 * ci, qa);
+        sm_store_quad<T>(C.q + 2 * ci + 1, qb);
+    }
+    if (!cached || pack) {  // CTA-uniform
+        // the packed record: in the position layout ring entries as positions (levels
+        // k .. k + 1 are positioned; an entry of level k + 2 keeps its id, flagged kUnres)
+        int dg = ((gl < d && rr.x < 0) || (gl + kGroup < d && rr.y < 0)) ? 1 : 0;
+        dg |= __shfl_xor_sync(kFull, dg, 1, kGroup);
+        dg |= __shfl_xor_sync(kFull, dg, 2, kGroup);
+        if (act && !ovf) {
+            int ea = rr.x, eb2 = rr.y;
+            if (posm) {
+                const int pa = hasa ? ldcg(posof + ida) : -1;
+                const int pb = hasb ? ldcg(posof + idb) : -1;
+                const int fa = rr.x & ~kIdMask, fb = rr.y & ~kIdMask;
+                ea = !hasa ? rr.x : pa >= 0 ? (fa | pa) : (fa | kUnres | ida);
+                eb2 = !hasb ? rr.y : pb >= 0 ? (fb | pb) : (fb | kUnres | idb);
+            }
+            const size_t N = static_cast<size_t>(A.stride);
+            const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
+            pring[s0] = ea;
+            pring[s1] = eb2;
+            pL[s0] = La;
+            pL[s1] = Lb;
+            qa.store_at(pquad, s0);
+            qb.store_at(pquad, s1);
+            if (gl == 0) pv[p] = v | kPacked | (dg ? kAlways : 0);
+        }
+    }
+    // overflow vertices (> 7 corners): the CSR ring, claims appended chunk by chunk
+    if (__any_sync(kFull, act && ovf)) {
+        int c0 = 0;
+        if (act && ovf) {
+            c0 = __ldg(M.cptr + v);
+            d = __ldg(M.cptr + v + 1) - c0;
+        }
+        const int r0 = c0 + v;
+        int nch = act && ovf ? (d + kEllW - 2) / (kEllW - 1) : 0;
+        nch = __reduce_max_sync(kFull, nch);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int base = ch * (kEllW - 1);
+            const int ea = base + gl, ebb = base + gl + kGroup;
+            const bool ha = act && ovf && ea <= d, hb = act && ovf && ebb <= d;
+            const int ia = ha ? __ldg(M.ring + r0 + ea) & INT_MAX : 0;
+            const int ib = hb ? __ldg(M.ring + r0 + ebb) & INT_MAX : 0;
+            const bool cA = ha && atomicCAS(level + ia, -1, lvl) == -1;
+            const bool cB = hb && atomicCAS(level + ib, -1, lvl) == -1;
+            claim_records<T>(cA, ia, cB, ib, M, CC.s_list, CC.g_list, CC.g_cap, CC.ccnt, CC.err);
         }
     }
 }
@@ -904,10 +1015,12 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         auto owned_count = [&](int first, int y) { return y > first ? div_nb(y - first + nb - 1) : 0; };
         int &sh_p0 = t0.sh_p0, &sh_a0 = t0.sh_a0, &sh_f0 = t0.sh_f0, &sh_fa0 = t0.sh_fa0,
             &sh_nfz = t0.sh_nfz;
+        int &sh_x0 = t0.sh_x0, &sh_xa0 = t0.sh_xa0;  // this CTA's first BFS task (next iteration)
         auto shares_now = [&] {
             first_owned(bb, sh_p0, sh_a0);
             first_owned(frzb, sh_f0, sh_fa0);
             sh_nfz = owned_count(sh_f0, frze);
+            if (bfs_open) first_owned(lim(k + 2), sh_x0, sh_xa0);  // level k + 2's BFS tasks
         };
         int& pf = t0.pf;
         int& be_pub = t0.be_pub;  // the band end publish() wrote to S.be (thread 0's copy)
@@ -931,23 +1044,47 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             S.j = j;
             S.bb = bb;
             S.fe = fe;
-            const int be = (bfs_open || j + 1 == rho) ? tail : lim(j + 1);
+            // the BFS runs one topleset ahead: levels through kk + 1 are positioned, so
+            // the band end lim(j + 1) is always known (lim(rho) = tail once it closed)
+            const int be = lim(j + 1);
             S.be = be;
             be_pub = be;
-            S.oe = bfs_open ? limk : be;  // newest topleset: records still in global memory
+            S.oe = j == kk ? lim(j) : be;  // the topleset relaxed for the first time
             S.expand = bfs_open;
+            // (sh_x0, sh_xa0) = first_owned(be): precomputed by thread 0 during the arrival
+            S.xe = bfs_open ? tail : be;
+            S.xp0 = bfs_open ? sh_x0 : be;  // no BFS tasks once the BFS has closed
+            S.xa0 = sh_xa0;
             S.frzb = frzb;
             S.frze = frze;
             S.parity = parity;
-            pf = -1;
-            if (i + 2 <= kk + 1 && (bfs_open || i + 2 <= rho))
-                pf = (bfs_open && i + 2 == kk + 1) ? tail : lim(i + 2);
             if (tr0) ctl->slot[(kk + 1) % 3] = 0ull;
             S.p0 = sh_p0;
             S.a0 = sh_a0;
             S.f0 = sh_f0;
             S.fa0 = sh_fa0;
             S.nfz = sh_nfz;
+        };
+
+        // BFS tasks of this CTA for the positions [xb, xe) (bfs4), claiming level `lvl`:
+        // narrow (cachedv) -- owned positions xp0 + t * nb into cache slots xa0 + t, from the
+        // top group down (the band's tasks fill the groups from the bottom up); wide -- chunks
+        // of 32 consecutive positions, records packed (ring entries as positions when posm)
+        auto bfs_loop = [&](bool cachedv, bool posm, int xb, int xe, int xp0, int xa0, int lvl) {
+            constexpr int kGroupsB = kB / kGroup;
+            for (int t = tid / kGroup;; t += kGroupsB) {
+                const int tb = cachedv ? kGroupsB - 1 - tid / kGroup + (t - tid / kGroup) : t;
+                const int p = cachedv ? xp0 + tb * nb
+                                      : xb + (lb + (t / 32) * nb) * 32 + (t % 32);
+                const bool act = p < xe;
+                if (!__any_sync(kFull, act)) break;
+                bool ca = false, cb = false;
+                int ia = 0, ib = 0;
+                bfs4<T>(M, A, C, (xa0 + tb) & (kCacheSlots - 1), act, cachedv, false, posm, p, lvl,
+                        pv, posof, pring, pL, pquad, level, CC, ca, ia, cb, ib);
+                claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap, CC.ccnt,
+                                 CC.err);
+            }
         };
 
         if (tid == 0) s_err = 0;
@@ -1049,8 +1186,41 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     }
                     done = (!bfs_open && i > rho - 1) || aborted(x);
                     shares_now();
-                    publish();
+                    // the BFS runs one topleset ahead: before iteration 1, claim level 2 from
+                    // the positions of level 1 [m, tail) (publish follows the pre-pass)
+                    S.done = done;
+                    S.expand = bfs_open && !done;
+                    S.xe = tail;
+                    first_owned(m, sh_x0, sh_xa0);
+                    S.xp0 = sh_x0;
+                    S.xa0 = sh_xa0;
+                    s_ccnt = 0;
                 });
+                if (S.expand) {
+                    const bool cpre = MODE == 1 ||
+                                      (MODE == 0 && A.wide_factor != 0 &&
+                                       S.xe - m <= (kCacheSlots - 1) * nb);
+                    bfs_loop(cpre, !LABELS, m, S.xe, S.xp0, S.xa0, 2);
+                    __syncthreads();
+                    const unsigned long long c2 = static_cast<unsigned long long>(s_ccnt);
+                    barrier((c2 << 32) | abort_bits(), S.xe, [] {}, [&](unsigned long long x) {
+                        const int tot = static_cast<int>(x >> 32);
+                        if (tot == 0) {
+                            bfs_open = 0;
+                            rho = 2;
+                        } else {
+                            tail += tot;
+                            set_lim(3, tail);
+                            if (lb == 0) limits[3] = tail;
+                        }
+                        done = aborted(x);
+                        first_owned(lim(2), sh_x0, sh_xa0);  // iteration 1's BFS tasks: level 2
+                        publish();
+                    });
+                } else {
+                    if (tid == 0) publish();
+                    __syncthreads();
+                }
             } else {
                 if (A.given_rho + 1 <= kLimRing) {
                     for (int r = tid; r <= A.given_rho; r += kB) s_lim[r] = ldcg(limits + r);
@@ -1076,7 +1246,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             // sequence (FPS rounds, batched fields) whose field is already complete
             // has nothing to do (every CTA reads the same ctl).
             if (__ldcg(&ctl->done)) return;
-            const int top = ctl->bfs_open ? ctl->k + 2 : ctl->rho;
+            const int top = ctl->bfs_open ? ctl->k + 3 : ctl->rho;  // BFS one topleset ahead
             const int lo = top - kLimRing + 1 > 0 ? top - kLimRing + 1 : 0;
             for (int r = lo + tid; r <= top; r += kB) s_lim[r % kLimRing] = ldcg(limits + r);
             __syncthreads();
@@ -1129,7 +1299,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         for (;;) {
             if (S.done || (A.max_iters > 0 && iters >= A.max_iters)) break;
             if constexpr (MODE != 0) {
-                const int span = S.be - S.bb;
+                const int span = S.xe - S.bb;  // the band and the BFS tasks' topleset
                 const bool wide = A.wide_factor == 0 || span > (kCacheSlots - 1) * nb;
                 if (MODE == 1 && wide) {
                     mode_exit = 2;
@@ -1151,11 +1321,12 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             const unsigned long long it0 = A.dbg != nullptr ? cyc() : 0ull;
             const int prv = S.parity, cur_b = prv ^ 1;
             const int bb_ = S.bb, be_ = S.be, fe_ = S.fe, oe_ = S.oe;
-            const bool expand = S.expand != 0;
+            // BFS tasks: positions [be, xe) (the topleset after the band's newest)
+            const int xe_ = S.xe, xp0_ = S.xp0, xa0_ = S.xa0;
             // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
             const bool cached = MODE == 1   ? true
                                 : MODE == 2 ? false
-                                            : A.wide_factor != 0 && (be_ - bb_) <= (kCacheSlots - 1) * nb;
+                                            : A.wide_factor != 0 && (xe_ - bb_) <= (kCacheSlots - 1) * nb;
             // single-source fields relax wide bands in the position layout; labelled ones
             // keep the id layout (measured: the 2048^2 height field's band does not fit L2,
             // and its row-major ids give each vertex's gathers shared sectors)
@@ -1163,9 +1334,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             if ((posl ? 1 : 0) != layout) relayout(posl ? 1 : 0);
             const CellT* cp = posl ? pcells[prv] : cells[prv];
             CellT* ccur = posl ? pcells[cur_b] : cells[cur_b];
-            // id layout: records are packed (ring ids) from the first relaxation once the
-            // band approaches the record cache's capacity, ready for the wide path
-            const bool pack = !kPosLayout && 2 * (be_ - bb_) > (kCacheSlots - 1) * nb;
+            // records are also packed by the BFS tasks of narrow iterations once the band
+            // approaches the record cache's capacity, ready for the wide path
+            const bool pack = 2 * (xe_ - bb_) > (kCacheSlots - 1) * nb;
             int* dnext = posl ? dflag + ((kk + 1) & 1) * n : nullptr;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
@@ -1186,24 +1357,29 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
                 const bool act = p0 + t * nb < be_;
                 const bool frz = tf < nfz;
-                if (!__any_sync(kFull, act || frz)) break;
+                const bool bact = xp0_ + tf * nb < xe_;  // BFS tasks from the top group down
+                if (!__any_sync(kFull, act || frz || bact)) break;
                 const int p = p0 + t * nb;
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
+                if (__any_sync(kFull, bact)) {
+                    bfs4<T>(M, A, C, (xa0_ + tf) & (kCacheSlots - 1), bact, true, pack,
+                            kPosLayout, xp0_ + tf * nb, kk + 2, pv, posof, pring, pL, pquad,
+                            level, CC, ca, ia, cb, ib);
+                    claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
+                                     CC.ccnt, CC.err);
+                }
                 unsigned long long* kd =
                     (A.dbg != nullptr && S.k - 1 < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
                      (tid & (kGroup - 1)) == 0)
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
-                relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, act && p >= oe_,
-                                  true, pack, false, p, kk, pv, posof, pring, pL, pquad, nullptr, cp,
-                                  ccur, fe_,
-                                  expand, level, eps, CC, nonconv, my_max, calls, degs, ca, ia,
-                                  cb, ib, (dbg && t == 0) ? dslot : nullptr,
-                                  kd, it0);
-                if (expand)
-                    claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
-                                     CC.ccnt, CC.err);
+                if (__any_sync(kFull, act))
+                    relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, false, true,
+                                      false, false, p, kk, pv, posof, pring, pL, pquad, nullptr,
+                                      cp, ccur, fe_, false, level, eps, CC, nonconv, my_max,
+                                      calls, degs, ca, ia, cb, ib,
+                                      (dbg && t == 0) ? dslot : nullptr, kd, it0);
                 if (kd) kd[9] = cyc() - it0;
                 if (frz && (tid & (kGroup - 1)) == 0) {
                     // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
@@ -1222,7 +1398,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             int* wq_v = wq_p + qcap;
             int* wq_r = wq_v + qcap;  // entry e of queued position x at wq_r[e * qcap + x]
             // this CTA's older positions: chunks lb, lb + nb, ... of 32 from bb up to oe
-            const int span0 = oe_ - bb_ - lb * kChunk;
+            const int span0 = be_ - bb_ - lb * kChunk;
             const int nch = span0 > 0 ? (span0 + nb * kChunk - 1) / (nb * kChunk) : 0;
             const int total = nch * kChunk;
             // (a CTA share beyond the queue's capacity relaxes every position this iteration)
@@ -1257,7 +1433,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         vr[u] = df[u] = 0;
 #pragma unroll
                         for (int e = 0; e < kEllW; ++e) rw[u][e] = 0;
-                        if (t < total && pp[u] < oe_) {
+                        if (t < total && pp[u] < be_) {
                             vr[u] = ldcg(pv + pp[u]);
                             df[u] = ldcg(dcur + pp[u]);
 #pragma unroll
@@ -1268,8 +1444,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
                         const int t = t0 + u * kB + tid;
-                        const bool in = t < total && pp[u] < oe_;
-                        const bool dirty = in && (fresh || !(vr[u] & kPacked) ||
+                        const bool in = t < total && pp[u] < be_;
+                        // the band's newest topleset is relaxed for the first time
+                        const bool dirty = in && (fresh || pp[u] >= oe_ || !(vr[u] & kPacked) ||
                                                   (vr[u] & kAlways) || df[u] == kk);
                         if (in && !dirty) calls += (rw[u][0] >> kMetaShift) & 7;
                         const unsigned bal = __ballot_sync(kFull, dirty);
@@ -1287,26 +1464,20 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 __syncthreads();
             }
             for (int t = tid / kGroup, tf = kGroups - 1 - tid / kGroup;; t += kGroups, tf += kGroups) {
-                // the newest topleset here, older ones one vertex per thread below (relax_wide2)
-                const int p = oe_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
-                const bool act = p < be_;
+                // BFS tasks here (the topleset after the band's newest, records packed),
+                // the band one vertex per thread below (relax_wide2)
+                const int p = be_ + (lb + (t / kChunk) * nb) * kChunk + (t % kChunk);
+                const bool act = p < xe_;
                 const bool frz = tf < nfz;
                 if (!__any_sync(kFull, act || frz)) break;
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
-                unsigned long long* kd =
-                    (A.dbg != nullptr && S.k - 1 < A.dbg_iters && act && p >= oe_ && p - nb < oe_ &&
-                     (tid & (kGroup - 1)) == 0)
-                        ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
-                        : nullptr;
-                relax4<T, LABELS>(M, A, C, 0, act, act, false, true, kPosLayout, p, kk, pv, posof, pring, pL,
-                                  pquad, dnext, cp, ccur,
-                                  fe_, expand, level, eps, CC, nonconv, my_max, calls, degs, ca,
-                                  ia, cb, ib, (dbg && t == 0) ? dslot : nullptr, kd, it0);
-                if (expand)
+                if (__any_sync(kFull, act)) {
+                    bfs4<T>(M, A, C, 0, act, false, false, kPosLayout, p, kk + 2, pv, posof,
+                            pring, pL, pquad, level, CC, ca, ia, cb, ib);
                     claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
                                      CC.ccnt, CC.err);
-                if (kd) kd[9] = cyc() - it0;
+                }
                 if (frz && (tid & (kGroup - 1)) == 0) {
                     // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
                     const int fp = f0 + tf * nb;
@@ -1371,8 +1542,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                     if constexpr (LABELS || sizeof(T) == 8) {
                         for (;; t = next_t(t)) {
                             p = pos(t);
-                            if (p - (t % kChunk) >= oe_) break;
-                            if (p < oe_) {
+                            if (p - (t % kChunk) >= be_) break;
+                            if (p < be_) {
                                 wide_pre(p, N, pv, pring, nx);
                                 relax_wide2<T, LABELS, kPosLayout>(M, A, p, kk, nx, pv, pring, pL, pquad,
                                                        posof, dnext, cp, ccur, fe_, eps, nonconv,
@@ -1380,14 +1551,14 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                             }
                         }
                     } else {
-                    if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
-                    while (p - (t % kChunk) < oe_) {
+                    if (p - (t % kChunk) < be_ && p < be_) wide_pre(p, N, pv, pring, nx);
+                    while (p - (t % kChunk) < be_) {
                         const WidePre cw = nx;
                         const int pc = p;
                         t = next_t(t);
                         p = pos(t);
-                        if (p - (t % kChunk) < oe_ && p < oe_) wide_pre(p, N, pv, pring, nx);
-                        if (pc < oe_)
+                        if (p - (t % kChunk) < be_ && p < be_) wide_pre(p, N, pv, pring, nx);
+                        if (pc < be_)
                             relax_wide2<T, LABELS, kPosLayout>(M, A, pc, kk, cw, pv, pring, pL, pquad, posof,
                                                    dnext, cp, ccur, fe_, eps, nonconv, my_max, calls,
                                                    degs);
@@ -1407,9 +1578,10 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             const unsigned long long pay = (nonconv ? (1ull << 16) : 0ull) | abort_bits() |
                                            (static_cast<unsigned long long>(s_ccnt) << 32);
             int c_p0 = 0, c_a0 = 0, n_p0 = 0, n_a0 = 0, c_nfz = 0;
-            barrier(pay, be_, [&] {
+            barrier(pay, xe_, [&] {  // claims: the topleset starting at xe
                 first_owned(fe, c_p0, c_a0);  // converged: the band starts at fe
                 first_owned(bb, n_p0, n_a0);  // not converged: it stays at bb
+                first_owned(tail, sh_x0, sh_xa0);  // next BFS tasks start at the current tail
                 c_nfz = owned_count(n_p0, fe);  // converged: [bb, fe) is frozen next
             }, [&](unsigned long long x) {
                 if (dbg) dslot[2] = gtimer();
@@ -1429,23 +1601,23 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         A.trace[row] = r;
                     }
                 }
+                // the claims of this iteration are level kk + 2 (one topleset ahead)
                 int nt = tail;
                 if (bfs_open) {
                     if (tot == 0) {
                         bfs_open = 0;
-                        rho = kk + 1;
+                        rho = kk + 2;
                     } else {
                         nt = tail + tot;
-                        set_lim(kk + 2, nt);
-                        if (lb == 0) limits[kk + 2] = nt;
-                        limk = tail;
+                        set_lim(kk + 3, nt);
+                        if (lb == 0) limits[kk + 3] = nt;
                     }
                 }
                 if (conv) {
                     frzb = bb;
                     frze = fe;
                     bb = fe;
-                    fe = (i + 2 <= kk + 1) ? pf : nt;
+                    fe = (bfs_open || i + 2 <= rho) ? lim(i + 2) : nt;
                     ++i;
                     sh_p0 = c_p0; sh_a0 = c_a0; sh_f0 = n_p0; sh_fa0 = n_a0; sh_nfz = c_nfz;
                 } else {
