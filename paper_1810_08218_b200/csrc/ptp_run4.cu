@@ -180,26 +180,18 @@ struct ClaimCtx {
     int* err;
 };
 
-// Relax the vertex at BFS position p (4-lane group; relax_vertex,
-// update_kernel.hpp:93-120).  Lanes return their claims in (ca, ia, cb, ib).
+// Relax the vertex at BFS position p (narrow iterations; 4-lane group; relax_vertex,
+// update_kernel.hpp:93-120): its record from the CTA's shared-memory cache (left there by
+// its BFS task, or by an earlier relaxation), or on a miss from the id-indexed ELL row;
+// the cells by vertex id.
 template <typename T, bool LABELS>
 __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const Cache<T>& C,
-                                       int sl, bool act, bool is_new, bool cached, bool pack,
-                                       bool posm,
-                                       int p, int kk, const int* pv, const int* posof,
-                                       int* pring, T* pL, char* pquad, int* dnext,
-                                       const Cell<T, LABELS>* cp,
-                                       Cell<T, LABELS>* cc, int fe, bool expand, int* level, T eps,
-                                       const ClaimCtx& CC, int& nonconv, T& my_max,
-                                       long long& calls, long long& degs, bool& ca_claim,
-                                       int& ida, bool& cb_claim, int& idb,
-                                       unsigned long long* tdbg,
-                                       unsigned long long* kdbg = nullptr,
-                                       unsigned long long it0 = 0) {
+                                       int sl, bool act, int p, int kk, const int* pv,
+                                       const Cell<T, LABELS>* cp, Cell<T, LABELS>* cc, int fe,
+                                       T eps, int& nonconv, T& my_max, long long& calls,
+                                       long long& degs, unsigned long long* tdbg) {
     const T inf = Lim<T>::inf();
     if (tdbg) tdbg[3] = cyc();
-    const unsigned long long k0 = kdbg ? cyc() : 0ull;
-    if (kdbg) kdbg[10] = k0 - it0;
     const int gl = threadIdx.x & (kGroup - 1);
     const int g0 = (threadIdx.x & 31) & ~(kGroup - 1);
     int v = 0;
@@ -210,7 +202,7 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
     qb = qa;
     const int ci = sl * 4 + gl;
     bool hit = false;
-    if (act && cached && !is_new) {
+    if (act) {
         const int2 tg = C.pv[ci];
         if (tg.x == p) {
             hit = true;
@@ -223,124 +215,57 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
         }
     }
     if (act && !hit) {
-        if (is_new) {
-            // the claimer's warp 0 writes pv[p] right after its barrier arrival
-            v = ld_relaxed_i32(pv + p);
-            for (int spin = 0; v < 0; ++spin) {
-                if (spin > (1 << 22)) {
-                    *CC.err = 3;
-                    v = 0;
-                    break;
-                }
-                v = ld_relaxed_i32(pv + p);
-            }
-            if (kdbg) kdbg[11] = gtimer_after(v) - k0;
-        } else {
-            v = ldcg(pv + p) & kIdMask;  // record-cache miss (first narrow iteration of a launch)
-        }
-        // the id-indexed ELL row (pulled into L2 by the claimer)
+        // cache miss (the first narrow iteration of a launch): position word, ELL row
+        v = ldcg(pv + p) & kIdMask;
         const size_t eb = static_cast<size_t>(v) * kEllW;
         rr = __ldg(reinterpret_cast<const int2*>(M.ering) + (eb >> 1) + gl);
         Ell2<T>::load(M.eL, eb + 2 * gl, La, Lb);
         qa.load(M.equad, static_cast<int>(eb + 2 * gl));
         qb.load(M.equad, static_cast<int>(eb + 2 * gl + 1));
-        if (cached) {
-            C.pv[ci] = make_int2(p, v);
-            C.rr[ci] = rr;
-            C.L[2 * ci] = La;
-            C.L[2 * ci + 1] = Lb;
-            sm_store_quad<T>(C.q + 2 * ci, qa);
-            sm_store_quad<T>(C.q + 2 * ci + 1, qb);
-        }
+        C.pv[ci] = make_int2(p, v);
+        C.rr[ci] = rr;
+        C.L[2 * ci] = La;
+        C.L[2 * ci + 1] = Lb;
+        sm_store_quad<T>(C.q + 2 * ci, qa);
+        sm_store_quad<T>(C.q + 2 * ci + 1, qb);
     }
     if (tdbg) tdbg[4] = gtimer_after(rr.x + v);
-    if (kdbg) kdbg[12] = gtimer_after(rr.x + rr.y + __float_as_int(static_cast<float>(La + qa.q11 + qb.q11))) - k0;
     const int meta = __shfl_sync(kFull, rr.x, g0);
     int d = act ? (meta >> kMetaShift) & 15 : 0;
     const bool ovf = d == kEllOverflow;
-    ida = rr.x & kIdMask;
-    idb = rr.y & kIdMask;
+    const int ida = rr.x & kIdMask;
+    const int idb = rr.y & kIdMask;
     const bool hasa = act && !ovf && d > 0 && gl <= d;
     const bool hasb = act && !ovf && d > 0 && gl + kGroup <= d;
-    const bool exp = expand && is_new;
-    ca_claim = false;
-    cb_claim = false;
     T tv = inf;
     int lv = -1, sv = 0;
     T ta = inf, tb = inf;
     int la = -1, lb_ = -1;
-    // cells: by vertex id in narrow iterations, by BFS position in wide ones (the
-    // neighbours' positions from posof; a neighbour without one yet is in the topleset
-    // being claimed now, never relaxed: +inf)
-    const int sidx = posm ? p : v;
-    int pa = ida, pb_ = idb;
-    if (posm) {
-        pa = hasa ? ldcg(posof + ida) : -1;
-        pb_ = hasb ? ldcg(posof + idb) : -1;
-    }
     if (act && gl == 0) {
-        const Cell<T, LABELS> c = ld_cell(cp + sidx);
+        const Cell<T, LABELS> c = ld_cell(cp + v);
         tv = c.d;
         lv = c.lab();
         sv = c.stamp();
     }
-    if (hasa && pa >= 0) {
-        const Cell<T, LABELS> c = ld_cell(cp + pa);
+    if (hasa) {
+        const Cell<T, LABELS> c = ld_cell(cp + ida);
         ta = c.d;
         la = c.lab();
     }
-    if (hasb && pb_ >= 0) {
-        const Cell<T, LABELS> c = ld_cell(cp + pb_);
+    if (hasb) {
+        const Cell<T, LABELS> c = ld_cell(cp + idb);
         tb = c.d;
         lb_ = c.lab();
     }
-    // any degenerate corner of the vertex (bit 31 of the corner's first entry), for the
-    // packed record's kAlways flag (all lanes take part in the shuffles)
-    int dg = 0;
-    if (pack) {  // CTA-uniform
-        dg = ((gl < d && rr.x < 0) || (gl + kGroup < d && rr.y < 0)) ? 1 : 0;
-        dg |= __shfl_xor_sync(kFull, dg, 1, kGroup);
-        dg |= __shfl_xor_sync(kFull, dg, 2, kGroup);
-    }
-    if (pack && is_new && !ovf) {
-        // the packed record, written at the first relaxation from the ELL row the claimer
-        // pulled into L2: ring entries as positions (an entry without one yet keeps its id,
-        // flagged kUnres), |x|, quads; slots 2gl and 2gl+1 = entries gl and gl+4
-        const size_t N = static_cast<size_t>(A.stride);
-        const size_t s0 = (2 * gl) * N + p, s1 = (2 * gl + 1) * N + p;
-        const int fa = rr.x & ~kIdMask, fb = rr.y & ~kIdMask;
-        if (posm) {
-            pring[s0] = !hasa ? rr.x : pa >= 0 ? (fa | pa) : (fa | kUnres | ida);
-            pring[s1] = !hasb ? rr.y : pb_ >= 0 ? (fb | pb_) : (fb | kUnres | idb);
-        } else {
-            pring[s0] = rr.x;
-            pring[s1] = rr.y;
-        }
-        pL[s0] = La;
-        pL[s1] = Lb;
-        qa.store_at(pquad, s0);
-        qb.store_at(pquad, s1);
-        if (gl == 0) const_cast<int*>(pv)[p] = v | kPacked | (dg ? kAlways : 0);
-    }
-    // BFS claims (toplesets.cpp:44-52), issued after the distance loads: an atomic
-    // ahead of them in the memory pipeline would delay the loads
-    if (exp) {
-        if (hasa) ca_claim = atomicCAS(level + ida, -1, kk + 1) == -1;
-        if (hasb) cb_claim = atomicCAS(level + idb, -1, kk + 1) == -1;
-    }
     if (tdbg) tdbg[5] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv)));
-    if (kdbg) kdbg[13] = gtimer_after(__float_as_int(static_cast<float>(ta + tb + tv))) - k0;
     T best = gl == 0 ? tv : inf;
     int bidx = gl == 0 ? -1 : INT_MAX;
     int blab = gl == 0 ? lv : -1;
     chunk_candidates<T, LABELS>(gl, 0, ovf ? 0 : d, rr.x, rr.y, La, Lb, ta, tb, la, lb_, qa, qb,
                                 best, bidx, blab, degs);
     if (tdbg) tdbg[6] = gtimer_after(__float_as_int(static_cast<float>(best)));
-    if (kdbg) kdbg[14] = gtimer_after(__float_as_int(static_cast<float>(best))) - k0;
-    if (kdbg) kdbg[15] = gtimer_after(static_cast<int>(ca_claim) + static_cast<int>(cb_claim)) - k0;
 
-    // overflow vertices (> 7 corners): CSR tables, 7 corners per chunk; their
-    // claims are appended one by one (rare: valence > 7)
+    // overflow vertices (> 7 corners): CSR tables, 7 corners per chunk (rare: valence > 7)
     if (__any_sync(kFull, act && ovf)) {
         int c0 = 0;
         if (act && ovf) {
@@ -372,28 +297,19 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
                 if (ebb < d) QB.load(M.quad, c0 + ebb);
             }
             const int ia = xa & INT_MAX, ib = xb & INT_MAX;
-            bool cA = false, cB = false;
-            if (exp) {
-                if (ha) cA = atomicCAS(level + ia, -1, kk + 1) == -1;
-                if (hb) cB = atomicCAS(level + ib, -1, kk + 1) == -1;
-            }
-            const int pA = posm && ha ? ldcg(posof + ia) : ia;
-            const int pB = posm && hb ? ldcg(posof + ib) : ib;
-            if (ha && pA >= 0) {
-                const Cell<T, LABELS> c = ld_cell(cp + pA);
+            if (ha) {
+                const Cell<T, LABELS> c = ld_cell(cp + ia);
                 TA = c.d;
                 lA = c.lab();
             }
-            if (hb && pB >= 0) {
-                const Cell<T, LABELS> c = ld_cell(cp + pB);
+            if (hb) {
+                const Cell<T, LABELS> c = ld_cell(cp + ib);
                 TB = c.d;
                 lB = c.lab();
             }
             const int dlim = act && ovf ? min(d, base + kEllW - 1) : 0;
             chunk_candidates<T, LABELS>(gl, base, dlim, xa, xb, LA, LB, TA, TB, lA, lB, QA, QB,
                                         best, bidx, blab, degs);
-            claim_records<T>(cA, ia, cB, ib, M, CC.s_list, CC.g_list, CC.g_cap, CC.ccnt,
-                             CC.err);
         }
     }
 
@@ -408,27 +324,10 @@ __device__ __forceinline__ void relax4(const MeshDev& M, const RunArgs& A, const
             if (LABELS) blab = ol;
         }
     }
-    if (posm && worklist_for<T>() && dnext != nullptr) {
-        // worklist marks: a changed vertex and its positioned neighbours are relaxed next
-        // iteration (neighbours without a position are the next newest topleset)
-        const bool chg = __shfl_sync(kFull, static_cast<int>(act && best != tv), g0) != 0;
-        if (chg) {
-            if (gl == 0) mark(dnext, p, kk);
-            if (hasa && pa >= 0) mark(dnext, pa, kk);
-            if (hasb && pb_ >= 0) mark(dnext, pb_, kk);
-            if (ovf && gl == 0) {
-                const int c0 = __ldg(M.cptr + v), r0 = c0 + v;
-                for (int e = 0; e <= d; ++e) {
-                    const int q = ldcg(posof + (__ldg(M.ring + r0 + e) & INT_MAX));
-                    if (q >= 0) mark(dnext, q, kk);
-                }
-            }
-        }
-    }
     if (act && gl == 0) {
         // the change stamp: this iteration if the distance changed (a label changes
         // only with its distance, update_kernel.hpp:114-117)
-        st_cell(cc + sidx, make_cell<T, LABELS>(best, blab, best != tv ? kk : sv));
+        st_cell(cc + v, make_cell<T, LABELS>(best, blab, best != tv ? kk : sv));
         calls += d;
         if (p < fe || A.last_change != nullptr) {
             const T rc = rel_change(tv, best);
@@ -1375,11 +1274,9 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
                 if (__any_sync(kFull, act))
-                    relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, false, true,
-                                      false, false, p, kk, pv, posof, pring, pL, pquad, nullptr,
-                                      cp, ccur, fe_, false, level, eps, CC, nonconv, my_max,
-                                      calls, degs, ca, ia, cb, ib,
-                                      (dbg && t == 0) ? dslot : nullptr, kd, it0);
+                    relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, p, kk, pv, cp,
+                                      ccur, fe_, eps, nonconv, my_max, calls, degs,
+                                      (dbg && t == 0) ? dslot : nullptr);
                 if (kd) kd[9] = cyc() - it0;
                 if (frz && (tid & (kGroup - 1)) == 0) {
                     // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
