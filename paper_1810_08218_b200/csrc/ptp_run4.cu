@@ -1,30 +1,26 @@
-// v4 PTP solver (sm_100a): stable position ownership, on-chip record cache,
-// payload-carrying grid barrier.
+// The PTP solver (sm_100a): the band loop of run_impl<T> (reference src/ptp.cpp:79-132) with
+// compute_toplesets' BFS (src/toplesets.cpp:37-55) fused in, as one persistent cooperative
+// kernel per field (or per group of concurrent fields), bit-identical to the reference.
+// Where every dependent memory trip of an iteration goes:
 //
-// Same semantics as ptp_run_kernel / ptp_run3_kernel (the band loop of
-// run_impl<T>, reference src/ptp.cpp:79-132, with compute_toplesets'
-// BFS, src/toplesets.cpp:37-55, fused in) and the same arithmetic
-// (corner_candidate / chunk_candidates), so results are bit-identical.  What
-// changes is where every dependent memory trip of an iteration goes:
-//
-//  * BFS position p of a query is owned by CTA p % nb for the whole solve.  The
-//    owner reads a vertex's record (ELL ring ids, |x|, Gram quads) once, at the
-//    vertex's first relaxation, from the id-indexed ELL tables the claimer pulled
-//    into L2 (prefetch.global.L2 at the claim), and keeps it in shared memory for
-//    every later iteration (a ring of R slots, slot p / nb).  An old band vertex
-//    therefore costs one L2 trip per iteration: the neighbour distances.
-//  * claims go to a per-CTA list; their BFS positions are assigned by the grid
-//    barrier itself: the arrival is one atom.acq_rel.add of a 64-bit word whose
-//    fields carry the iteration's payload (bits 0-15 arrivals, 16-31 CTAs with a
-//    front change >= eps, ptp.cpp:107,114, 32-63 claims = the next topleset's
-//    size); the value it returns is the CTA's offset in the new topleset, and
-//    warp 0 writes the list to pv[] while the CTA waits.  Topleset limits live in
-//    a shared-memory ring, so polling that word is the only trip after the barrier.
-//  * wide iterations (band beyond the record cache; MODE 2 when launched narrow /
-//    wide separately) deal positions in chunks of 32 and relax one vertex per
-//    thread from records packed by position (slot-major, reorder_for_bands layout,
-//    toplesets.cpp:60-89), written by the owner at the first relaxation once the
-//    band approaches the cache's capacity.
+//  * the BFS runs one topleset ahead of the band: at iteration k a BFS task per position of
+//    level k+1 reads the vertex's ELL row (pulled into L2 by its claimer) into the owner's
+//    record cache (narrow iterations) or its packed record (wide ones) and claims level k+2
+//    (bfs4); level k+1 is relaxed for the first time at iteration k+1 from the chip.
+//  * narrow iterations (MODE 1): BFS position p is owned by CTA p % nb for the whole solve
+//    and its record lives in the owner's shared-memory cache (slot p / nb), so a band vertex
+//    costs one L2 trip per iteration: its neighbours' cells (by vertex id).
+//  * claims go to a per-CTA list; their BFS positions are assigned by the grid barrier
+//    itself: the arrival is one atom.acq_rel.add of a 64-bit word whose fields carry the
+//    iteration's payload (bits 0-15 arrivals, 16-31 CTAs with a front change >= eps,
+//    ptp.cpp:107,114, 32-63 claims = the next topleset's size); the value it returns is the
+//    CTA's offset in the new topleset, and warp 0 writes the list to pv[] / posof[] while
+//    the CTA waits.  Topleset limits live in a shared-memory ring.
+//  * wide iterations (MODE 2; band beyond the record cache) relax one vertex per thread in
+//    chunks of 32 positions from records packed by position (slot-major, the
+//    reorder_for_bands layout, toplesets.cpp:60-89); single-source fields keep their cells
+//    by BFS position there (relayout), and fp64 ones relax only the positions a change
+//    marked (the change-driven worklist).
 #include "ptp_common.cuh"
 #include "ptp_launch.hpp"
 
@@ -1389,7 +1385,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             {
                 // older band positions [bb, oe): one vertex per thread, chunked.  Warps
                 // take this CTA's chunks from a shared counter, so the warps that held the
-                // newest topleset's tasks (BFS claims: the longest chain) take fewer.
+                // BFS tasks (the longest chain) take fewer.
                 // Chunk m of this CTA starts at position bb + (lb + m * nb) * 32; task t
                 // below is chunk * 32 + lane.
                 const int lane = tid & 31;
