@@ -77,6 +77,13 @@ struct Bcast4 {
 };
 
 constexpr int kCacheSlots = 512;  // record-cache ring (power of two) per CTA
+#ifndef GEODIST_NARROW_MAX
+#define GEODIST_NARROW_MAX 256
+#endif
+// narrow iterations while the band (and the BFS tasks' topleset) spans at most this many
+// positions per CTA (<= kCacheSlots - 1, the record cache's capacity; 256 measured: wide
+// iterations from there are cheaper -- torus 12.82 -> 12.76 ms, height field 12.25 -> 11.83)
+constexpr int kNarrowMax = GEODIST_NARROW_MAX;
 
 __device__ __forceinline__ void red_release_u64(unsigned long long* p, unsigned long long x) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
@@ -1203,12 +1210,12 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             if (S.done || (A.max_iters > 0 && iters >= A.max_iters)) break;
             if constexpr (MODE != 0) {
                 const int span = S.xe - S.bb;  // the band and the BFS tasks' topleset
-                const bool wide = A.wide_factor == 0 || span > (kCacheSlots - 1) * nb;
+                const bool wide = A.wide_factor == 0 || span > kNarrowMax * nb;
                 if (MODE == 1 && wide) {
                     mode_exit = 2;
                     break;
                 }
-                if (MODE == 2 && A.wide_factor != 0 && 2 * span <= (kCacheSlots - 1) * nb) {
+                if (MODE == 2 && A.wide_factor != 0 && 2 * span <= kNarrowMax * nb) {
                     mode_exit = 1;  // narrow again (with hysteresis)
                     break;
                 }
@@ -1229,7 +1236,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             // GEODIST_WIDE=0 (wide_factor 0) forces the wide path (tests)
             const bool cached = MODE == 1   ? true
                                 : MODE == 2 ? false
-                                            : A.wide_factor != 0 && (xe_ - bb_) <= (kCacheSlots - 1) * nb;
+                                            : A.wide_factor != 0 && (xe_ - bb_) <= kNarrowMax * nb;
             // single-source fields relax wide bands in the position layout; labelled ones
             // keep the id layout (measured: the 2048^2 height field's band does not fit L2,
             // and its row-major ids give each vertex's gathers shared sectors)
@@ -1239,7 +1246,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             CellT* ccur = posl ? pcells[cur_b] : cells[cur_b];
             // records are also packed by the BFS tasks of narrow iterations once the band
             // approaches the record cache's capacity, ready for the wide path
-            const bool pack = 2 * (xe_ - bb_) > (kCacheSlots - 1) * nb;
+            const bool pack = 2 * (xe_ - bb_) > kNarrowMax * nb;
             int* dnext = posl ? dflag + ((kk + 1) & 1) * n : nullptr;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
