@@ -52,7 +52,13 @@ constexpr int kAlways = 1 << 29;
 // previous iteration (see the older-band loop); 0: every band position every iteration.
 // fp64 only: measured on the 1000^2 torus, fp64 17.3 ms with it vs 18.7 without, fp32
 // 15.3 vs 14.6 -- the scan trip costs more than the skipped fp32 relaxations save.
-template <typename T> __host__ __device__ constexpr bool worklist_for() { return GEODIST_WORKLIST != 0 && sizeof(T) == 8; }
+#ifndef GEODIST_WL_MASK
+#define GEODIST_WL_MASK 4  // bit 0: fp32 single source, 1: fp32 labels, 2: fp64 single, 3: fp64 labels
+#endif
+template <typename T, bool L> __host__ __device__ constexpr bool worklist_for() {
+    return GEODIST_WORKLIST != 0 &&
+           ((GEODIST_WL_MASK >> ((sizeof(T) == 8 ? 2 : 0) + (L ? 1 : 0))) & 1) != 0;
+}
 
 // Mark position q for relaxation in the next iteration (mark value kk + 1 in the array
 // of the next iteration's parity).  Plain stores: every writer stores the same value.
@@ -719,19 +725,28 @@ __device__ __forceinline__ void relax_wide2(const MeshDev& M, const RunArgs& A, 
         }
     }
     calls += d;
-    if (POS && worklist_for<T>() && best != tv) {
+    if (worklist_for<T, LABELS>() && dnext != nullptr && best != tv) {
         // worklist marks for the next iteration: this vertex and its positioned neighbours
+        // (in the id layout their positions from posof: a neighbour without one yet is the
+        // next newest topleset, relaxed anyway)
         mark(dnext, p, kk);
         if (ovfl) {
             const int r0 = __ldg(M.cptr + v) + v;
             for (int e = 0; e <= d; ++e) {
-                const int q = ldcg(posof + (__ldg(M.ring + r0 + e) & INT_MAX));
+                const int q = ld_c(posof + (__ldg(M.ring + r0 + e) & INT_MAX));
                 if (q >= 0) mark(dnext, q, kk);
             }
-        } else {
+        } else if (POS) {
 #pragma unroll
             for (int e = 0; e < kEllW; ++e)
                 if (e <= d && !((unk >> e) & 1u)) mark(dnext, raw[e] & kIdMask, kk);
+        } else {
+            int q[kEllW];
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e) q[e] = e <= d ? ld_c(posof + (raw[e] & kIdMask)) : -1;
+#pragma unroll
+            for (int e = 0; e < kEllW; ++e)
+                if (q[e] >= 0) mark(dnext, q[e], kk);
         }
     }
     // The other buffer holds this vertex's cell of two iterations ago: rewrite it only
@@ -1177,7 +1192,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         // are positions).  Every launch starts and ends in the id layout; crossing over
         // is one pass over the positions assigned so far, both buffers, and a barrier.
         int layout = 0;
-        bool fresh = false;
+        bool fresh = false, was_wide = false;
 
         auto relayout = [&](int to) {
             const int top = S.tail;
@@ -1196,7 +1211,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 }
             }
             // wide iterations reuse the record cache's shared memory as the worklist queue
-            if (to == 0 && kPosLayout && worklist_for<T>())
+            if (to == 0 && kPosLayout && worklist_for<T, LABELS>())
                 for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
             barrier(0ull, 0, [] {}, [](unsigned long long) {});
             layout = to;
@@ -1247,7 +1262,18 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             // records are also packed by the BFS tasks of narrow iterations once the band
             // approaches the record cache's capacity, ready for the wide path
             const bool pack = 2 * (xe_ - bb_) > kNarrowMax * nb;
-            int* dnext = posl ? dflag + ((kk + 1) & 1) * n : nullptr;
+            int* dnext = (!cached && worklist_for<T, LABELS>()) ? dflag + ((kk + 1) & 1) * n : nullptr;
+            // the first wide iteration after narrow ones has no marks: it relaxes every position;
+            // narrow ones after wide ones (combined instantiation, id layout) find the record
+            // cache's memory used as the worklist queue: its tags are reset
+            if (!cached && !was_wide) fresh = true;
+            if constexpr (worklist_for<T, LABELS>() && !kPosLayout) {
+                if (cached && was_wide) {
+                    for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
+                    __syncthreads();
+                }
+            }
+            was_wide = !cached;
             // owned positions: band task t at p0 + t * nb; the frozen topleset's
             // positions go to the groups from the top of the CTA down
             const int p0 = S.p0, a0 = S.a0;
@@ -1310,7 +1336,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             const int nch = span0 > 0 ? (span0 + nb * kChunk - 1) / (nb * kChunk) : 0;
             const int total = nch * kChunk;
             // (a CTA share beyond the queue's capacity relaxes every position this iteration)
-            const bool wl = kPosLayout && worklist_for<T>() && total <= qcap;
+            const bool wl = worklist_for<T, LABELS>() && total <= qcap;
             if (wl) {
                 // Change-driven worklist (position layout).  relax_vertex is a pure function
                 // of the neighbours' previous values and starts from the vertex's own previous
