@@ -65,10 +65,10 @@ template <typename T, bool L> __host__ __device__ constexpr bool worklist_for() 
 __device__ __forceinline__ void mark(int* dnext, int q, int kk) { dnext[q] = kk + 1; }
 
 struct T0State {
-    int k, i, rho, parity, bfs_open, done, tail, limk, bb, fe, frzb, frze, lim_top;
+    int k, i, rho, parity, bfs_open, done, tail, bb, fe, frzb, frze, lim_top;
     bool use_glim;
     unsigned long long upd;
-    int sh_p0, sh_a0, sh_f0, sh_fa0, sh_nfz, pf, be_pub, sh_x0, sh_xa0;
+    int sh_p0, sh_a0, sh_f0, sh_fa0, sh_nfz, be_pub, sh_x0, sh_xa0;
 };
 
 struct Bcast4 {
@@ -903,14 +903,14 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         }();
         int &k = t0.k, &i = t0.i, &rho = t0.rho, &parity = t0.parity, &bfs_open = t0.bfs_open,
             &done = t0.done;
-        int &tail = t0.tail, &limk = t0.limk, &bb = t0.bb, &fe = t0.fe, &frzb = t0.frzb,
+        int &tail = t0.tail, &bb = t0.bb, &fe = t0.fe, &frzb = t0.frzb,
             &frze = t0.frze;
         int& lim_top = t0.lim_top;    // highest topleset limit index held in s_lim
         bool& use_glim = t0.use_glim; // limits read from global memory (ring too short)
         unsigned long long& upd = t0.upd;
         if (tid == 0) {
             k = 0; i = 1; rho = INT_MAX; parity = 0; bfs_open = 0; done = 0;
-            tail = 0; limk = 0; bb = 0; fe = 0; frzb = 0; frze = 0;
+            tail = 0; bb = 0; fe = 0; frzb = 0; frze = 0;
             lim_top = -1;
             use_glim = false;
             upd = 0;
@@ -947,10 +947,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             sh_nfz = owned_count(sh_f0, frze);
             if (bfs_open) first_owned(lim(k + 2), sh_x0, sh_xa0);  // level k + 2's BFS tasks
         };
-        int& pf = t0.pf;
         int& be_pub = t0.be_pub;  // the band end publish() wrote to S.be (thread 0's copy)
         if (tid == 0) {
-            pf = -1;
             be_pub = 0;
         }
         const bool tr0 = A.trace != nullptr && lb == 0;
@@ -1103,7 +1101,6 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         fe = m;
                     } else {
                         bfs_open = 1;
-                        limk = m;
                         tail = m + tot;
                         fe = tail;
                         set_lim(2, tail);
@@ -1178,7 +1175,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
             if (tid == 0) {
                 k = ctl->k; i = ctl->i; rho = ctl->rho; parity = ctl->parity;
                 bfs_open = ctl->bfs_open; done = ctl->done;
-                tail = ctl->s_tail; limk = ctl->s_limk; bb = ctl->s_bb; fe = ctl->s_fe;
+                tail = ctl->s_tail; bb = ctl->s_bb; fe = ctl->s_fe;
                 frzb = ctl->s_frzb; frze = ctl->s_frze;
                 lim_top = top;
                 shares_now();
@@ -1580,7 +1577,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 ctl->k = k; ctl->i = i; ctl->rho = rho; ctl->parity = parity;
                 ctl->bfs_open = bfs_open; ctl->done = done;
                 ctl->mode_exit = mode_exit;
-                ctl->s_tail = tail; ctl->s_limk = limk; ctl->s_bb = bb; ctl->s_fe = fe;
+                ctl->s_tail = tail; ctl->s_bb = bb; ctl->s_fe = fe;
                 ctl->s_frzb = frzb; ctl->s_frze = frze;
                 ctl->updates += upd;
             }
