@@ -229,8 +229,11 @@ static const void* run_kernel_ptr(int mode, int precision, bool labels) {
 int run_max_blocks(int precision, bool labels, int device, int mode) {
     int per_sm = 0, sms = 0;
     const void* f = run_kernel_ptr(mode, precision, labels);
-    const size_t dyn = run4_dyn_smem(precision, labels);
+    const size_t dyn = run4_dyn_smem(precision, labels, mode);
     if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    // without dynamic shared memory (the wide-only instantiation) the rest of the SM's
+    // 256 KB goes to L1, which caches the cell gathers
+    if (!dyn) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, run4_block(mode), dyn);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     // a group's CTA count must fit the barrier word's 8-bit-safe nonconverged-CTA
@@ -248,8 +251,9 @@ cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStre
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const void* f = run_kernel_ptr(mode, precision, labels);
-    const size_t dyn = run4_dyn_smem(precision, labels);
+    const size_t dyn = run4_dyn_smem(precision, labels, mode);
     if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (!dyn) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     e = cudaLaunchCooperativeKernel(f, dim3(grid), dim3(run4_block(mode)), params, dyn, st);
     note_launch();
     return e;

@@ -27,7 +27,7 @@ void launch_arith_selftest(long long n, unsigned long long seed, unsigned long l
 // Max co-resident CTAs of the run kernel on `device` (cooperative launch bound).
 int run_max_blocks(int precision, bool labels, int device, int mode = 0);
 // record-cache bytes (dynamic shared memory) and kernel entry
-size_t run4_dyn_smem(int precision, bool labels);
+size_t run4_dyn_smem(int precision, bool labels, int mode);
 const void* run4_kernel_ptr(int precision, bool labels, int mode = 0);
 cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStream_t st,
                        int mode = 0);

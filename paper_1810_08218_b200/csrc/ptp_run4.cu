@@ -883,8 +883,11 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         return static_cast<int>((x >> 16) & 0xffffull) > nb;
     };
 
-    // reset the record cache tags (smem does not survive launches)
-    for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
+    // reset the record cache tags (smem does not survive launches); the wide-only
+    // instantiation has no record cache (and no dynamic shared memory unless its worklist
+    // queue needs it: the rest goes to L1, which caches the cell gathers)
+    if constexpr (MODE != 2)
+        for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
 
     for (int q = g; q < A.nq; q += A.groups) {
         const int s0 = A.src_off ? A.src_off[q] : 0;
@@ -1011,7 +1014,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
         };
 
         if (tid == 0) s_err = 0;
-        if (q != g)
+        if (MODE != 2 && q != g)
             for (int x = tid; x < 4 * R; x += kB) C.pv[x] = make_int2(-1, 0);
         if (A.phase_init) {
             // reset (ptp.cpp:61-68)
@@ -1671,9 +1674,17 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
 // ---------------------------------------------------------------------------
 // host side
 
-size_t run4_dyn_smem(int precision, bool) {
-    return kCacheSlots *
-           (precision == 0 ? Cache<float>::bytes_per_slot() : Cache<double>::bytes_per_slot());
+size_t run4_dyn_smem(int precision, bool labels, int mode) {
+    const size_t cache = kCacheSlots * (precision == 0 ? Cache<float>::bytes_per_slot()
+                                                       : Cache<double>::bytes_per_slot());
+    if (mode == 2) {  // wide-only: the worklist queue (record cache memory) or nothing
+        const bool wl = precision == 0 ? (labels ? worklist_for<float, true>()
+                                                 : worklist_for<float, false>())
+                                       : (labels ? worklist_for<double, true>()
+                                                 : worklist_for<double, false>());
+        return wl ? cache : 0;
+    }
+    return cache;
 }
 
 template <int MODE> static const void* run4_ptr(int precision, bool labels) {
