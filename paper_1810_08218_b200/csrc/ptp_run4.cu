@@ -39,7 +39,7 @@ constexpr int kPacked = 1 << 30;
 // iteration); resolved through posof at a later relaxation.  Bit 30 is free in every
 // entry of a packed record (entry 0's corner-count field is <= 7 there).
 #ifndef GEODIST_POSL
-#define GEODIST_POSL 1
+#define GEODIST_POSL 0
 #endif
 constexpr int kUnres = 1 << 30;
 // pv[p] flag: the vertex has a degenerate corner (its degenerate_calls count depends on
@@ -53,7 +53,7 @@ constexpr int kAlways = 1 << 29;
 // fp64 only: measured on the 1000^2 torus, fp64 17.3 ms with it vs 18.7 without, fp32
 // 15.3 vs 14.6 -- the scan trip costs more than the skipped fp32 relaxations save.
 #ifndef GEODIST_WL_MASK
-#define GEODIST_WL_MASK 4  // bit 0: fp32 single source, 1: fp32 labels, 2: fp64 single, 3: fp64 labels
+#define GEODIST_WL_MASK 0  // bit 0: fp32 single source, 1: fp32 labels, 2: fp64 single, 3: fp64 labels
 #endif
 template <typename T, bool L> __host__ __device__ constexpr bool worklist_for() {
     return GEODIST_WORKLIST != 0 &&
@@ -785,10 +785,11 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
 
     const int tid = threadIdx.x;
     constexpr int R = kCacheSlots;
-    // Wide iterations of fp64 single-source fields use the BFS-position layout (it carries
-    // the change-driven worklist: torus fp64 17.0 ms vs 19.0 in the id layout); fp32 and
-    // labelled fields keep the id layout, whose row-major neighbours share L1 lines
-    // (torus fp32 12.85 ms vs 13.92 by position, height field 12.05 vs 16.9)
+    // Wide iterations keep the cells by vertex id: with L1-cached gathers (and the wide-only
+    // instantiation's shared memory given to L1) row-major neighbours share L1 lines (torus
+    // fp32 12.7 ms vs 13.9 by position; fp64 14.6 ms vs 17.0 by position with the worklist).
+    // GEODIST_POSL=1 puts fp64 single-source fields in the BFS-position layout (with
+    // GEODIST_WL_MASK bit 2, the change-driven worklist), the round-2 alternative.
     constexpr bool kPosLayout = !LABELS && sizeof(T) == 8 && GEODIST_POSL;
     Cache<T> C;
     C.bind(dsm, R);
