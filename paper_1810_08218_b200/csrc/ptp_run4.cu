@@ -82,9 +82,12 @@ struct Bcast4 {
     int p0, a0, f0, fa0, nfz;
 };
 
-constexpr int kCacheSlots = 512;  // record-cache ring (power of two) per CTA
+#ifndef GEODIST_CACHE_SLOTS
+#define GEODIST_CACHE_SLOTS 256
+#endif
+constexpr int kCacheSlots = GEODIST_CACHE_SLOTS;  // record-cache ring (power of two) per CTA
 #ifndef GEODIST_NARROW_MAX
-#define GEODIST_NARROW_MAX 256
+#define GEODIST_NARROW_MAX (kCacheSlots - 1)
 #endif
 // narrow iterations while the band (and the BFS tasks' topleset) spans at most this many
 // positions per CTA (<= kCacheSlots - 1, the record cache's capacity; 256 measured: wide
