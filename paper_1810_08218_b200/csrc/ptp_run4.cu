@@ -82,17 +82,20 @@ struct Bcast4 {
     int p0, a0, f0, fa0, nfz;
 };
 
-#ifndef GEODIST_CACHE_SLOTS
-#define GEODIST_CACHE_SLOTS 256
+// Record-cache ring (power of two) per CTA; narrow iterations last while the band and the
+// BFS tasks' topleset span at most cache_slots - 1 positions per CTA.  The rest of the SM's
+// shared memory is L1 (cell gathers).  Measured (icosphere-8 / grid / torus / height):
+// fp32 128 slots 3.64 ms vs 256: 3.76 on the icosphere-8, the others equal; fp64 256 slots
+// 3.99 ms vs 128: 4.48 (its band spills to the wide path) and vs 512: 4.06.
+#ifndef GEODIST_CACHE_SLOTS32
+#define GEODIST_CACHE_SLOTS32 128
 #endif
-constexpr int kCacheSlots = GEODIST_CACHE_SLOTS;  // record-cache ring (power of two) per CTA
-#ifndef GEODIST_NARROW_MAX
-#define GEODIST_NARROW_MAX (kCacheSlots - 1)
+#ifndef GEODIST_CACHE_SLOTS64
+#define GEODIST_CACHE_SLOTS64 256
 #endif
-// narrow iterations while the band (and the BFS tasks' topleset) spans at most this many
-// positions per CTA (<= kCacheSlots - 1, the record cache's capacity; 256 measured: wide
-// iterations from there are cheaper -- torus 12.82 -> 12.76 ms, height field 12.25 -> 11.83)
-constexpr int kNarrowMax = GEODIST_NARROW_MAX;
+template <typename T> __host__ __device__ constexpr int cache_slots() {
+    return sizeof(T) == 4 ? GEODIST_CACHE_SLOTS32 : GEODIST_CACHE_SLOTS64;
+}
 
 __device__ __forceinline__ void red_release_u64(unsigned long long* p, unsigned long long x) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
@@ -787,7 +790,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
     __shared__ int s_qn, s_qh;  // worklist length / next batch (wide iterations)
 
     const int tid = threadIdx.x;
-    constexpr int R = kCacheSlots;
+    constexpr int R = cache_slots<T>();
+    constexpr int kNarrowMax = R - 1;
     // Wide iterations keep the cells by vertex id: with L1-cached gathers (and the wide-only
     // instantiation's shared memory given to L1) row-major neighbours share L1 lines (torus
     // fp32 12.7 ms vs 13.9 by position; fp64 14.6 ms vs 17.0 by position with the worklist).
@@ -1010,7 +1014,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 if (!__any_sync(kFull, act)) break;
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
-                bfs4<T>(M, A, C, (xa0 + tb) & (kCacheSlots - 1), act, cachedv, false, posm, p, lvl,
+                bfs4<T>(M, A, C, (xa0 + tb) & (R - 1), act, cachedv, false, posm, p, lvl,
                         pv, posof, pring, pL, pquad, level, CC, ca, ia, cb, ib);
                 claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap, CC.ccnt,
                                  CC.err);
@@ -1128,7 +1132,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 if (S.expand) {
                     const bool cpre = MODE == 1 ||
                                       (MODE == 0 && A.wide_factor != 0 &&
-                                       S.xe - m <= (kCacheSlots - 1) * nb);
+                                       S.xe - m <= (R - 1) * nb);
                     bfs_loop(cpre, kPosLayout, m, S.xe, S.xp0, S.xa0, 2);
                     __syncthreads();
                     const unsigned long long c2 = static_cast<unsigned long long>(s_ccnt);
@@ -1303,7 +1307,7 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                 bool ca = false, cb = false;
                 int ia = 0, ib = 0;
                 if (__any_sync(kFull, bact)) {
-                    bfs4<T>(M, A, C, (xa0_ + tf) & (kCacheSlots - 1), bact, true, pack,
+                    bfs4<T>(M, A, C, (xa0_ + tf) & (R - 1), bact, true, pack,
                             kPosLayout, xp0_ + tf * nb, kk + 2, pv, posof, pring, pL, pquad,
                             level, CC, ca, ia, cb, ib);
                     claim_records<T>(ca, ia, cb, ib, M, CC.s_list, CC.g_list, CC.g_cap,
@@ -1315,14 +1319,14 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
                         ? A.dbg + kDbgSlots * (static_cast<size_t>(S.k - 1) * gridDim.x + blockIdx.x)
                         : nullptr;
                 if (__any_sync(kFull, act))
-                    relax4<T, LABELS>(M, A, C, (a0 + t) & (kCacheSlots - 1), act, p, kk, pv, cp,
+                    relax4<T, LABELS>(M, A, C, (a0 + t) & (R - 1), act, p, kk, pv, cp,
                                       ccur, fe_, eps, nonconv, my_max, calls, degs,
                                       (dbg && t == 0) ? dslot : nullptr);
                 if (kd) kd[9] = cyc() - it0;
                 if (frz && (tid & (kGroup - 1)) == 0) {
                     // deferred freeze of the topleset retired last iteration (ptp.cpp:121-130)
                     const int fp = f0 + tf * nb;
-                    const int2 tg = C.pv[((fa0 + tf) & (kCacheSlots - 1)) * 4];
+                    const int2 tg = C.pv[((fa0 + tf) & (R - 1)) * 4];
                     const int v = tg.x == fp ? tg.y : (ldcg(pv + fp) & kIdMask);
                     st_cell(ccur + v, ld_cell(cp + v));
                 }
@@ -1679,8 +1683,8 @@ __global__ void __launch_bounds__(run4_block(MODE), 1) ptp_run4_kernel(RunArgs A
 // host side
 
 size_t run4_dyn_smem(int precision, bool labels, int mode) {
-    const size_t cache = kCacheSlots * (precision == 0 ? Cache<float>::bytes_per_slot()
-                                                       : Cache<double>::bytes_per_slot());
+    const size_t cache = precision == 0 ? cache_slots<float>() * Cache<float>::bytes_per_slot()
+                                        : cache_slots<double>() * Cache<double>::bytes_per_slot();
     if (mode == 2) {  // wide-only: the worklist queue (record cache memory) or nothing
         const bool wl = precision == 0 ? (labels ? worklist_for<float, true>()
                                                  : worklist_for<float, false>())
