@@ -231,9 +231,10 @@ int run_max_blocks(int precision, bool labels, int device, int mode) {
     const void* f = run_kernel_ptr(mode, precision, labels);
     const size_t dyn = run4_dyn_smem(precision, labels, mode);
     if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    // without dynamic shared memory (the wide-only instantiation) the rest of the SM's
-    // 256 KB goes to L1, which caches the cell gathers
-    if (!dyn) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    // prefer L1: the shared-memory carveout is then the smallest that fits the record cache
+    // (none in the wide-only instantiation), and the rest of the SM's 256 KB caches the cell
+    // gathers
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, run4_block(mode), dyn);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     // a group's CTA count must fit the barrier word's 8-bit-safe nonconverged-CTA
@@ -253,7 +254,7 @@ cudaError_t launch_run(int precision, bool labels, const RunArgs& args, cudaStre
     const void* f = run_kernel_ptr(mode, precision, labels);
     const size_t dyn = run4_dyn_smem(precision, labels, mode);
     if (dyn) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (!dyn) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     e = cudaLaunchCooperativeKernel(f, dim3(grid), dim3(run4_block(mode)), params, dyn, st);
     note_launch();
     return e;
