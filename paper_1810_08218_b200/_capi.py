@@ -10,7 +10,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgeodist_b200.so")
+# GEODIST_B200_LIB: another in-tree build of the same C ABI (the tests load the alternative
+# layouts' build, libgeodist_b200_alt.so, this way)
+LIB_PATH = os.environ.get("GEODIST_B200_LIB") or os.path.join(HERE, "libgeodist_b200.so")
 
 GEODIST_OK, GEODIST_EINVAL, GEODIST_EMESH, GEODIST_ECUDA, GEODIST_ENOMEM = range(5)
 
