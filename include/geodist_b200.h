@@ -251,6 +251,11 @@ int geodist_selftest_arith(int64_t n, uint64_t seed, int64_t* counts);
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t geodist_kernel_launches(void);
 
+/* Demote the L2 lines the solver's access-policy window marked persisting on the current
+ * device (cudaCtxResetPersistingL2Cache), so that a cache flush evicts them too (benchmarks
+ * that flush L2 between timed fields). */
+int geodist_reset_persisting_l2(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ EXPORTED = [
     "geodist_reorder_for_bands", "geodist_reorder_ordered", "geodist_ptp", "geodist_ptp_ordered",
     "geodist_voronoi",
     "geodist_fps", "geodist_batch_device", "geodist_batch", "geodist_planar_update",
-    "geodist_kernel_launches", "geodist_selftest_arith",
+    "geodist_kernel_launches", "geodist_selftest_arith", "geodist_reset_persisting_l2",
 ]
 
 

@@ -625,6 +625,9 @@ extern "C" {
 const char* geodist_last_error(void) { return g_err.c_str(); }
 int32_t geodist_version(void) { return 100; }
 int64_t geodist_kernel_launches(void) { return g_launches.load(); }
+int geodist_reset_persisting_l2(void) {
+    return guarded([&] { cuda_ok(cudaCtxResetPersistingL2Cache(), "reset persisting L2"); });
+}
 
 int geodist_device_count(int32_t* count) {
     return guarded([&] {
