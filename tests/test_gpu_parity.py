@@ -160,6 +160,9 @@ SYNTH = [
     # sized, so the field is abandoned (err 2) and redone with full-size lists; from
     # the centre (iteration-0 claims) and from a spoke (the centre claims at k = 1)
     ("wheel9000", lambda: polar_arrays(9000, 3), [[0], [7], [7, 20000]]),
+    # a first topleset wider than the narrow path's record cache on every CTA (20000 > 148 x
+    # 127): the BFS pre-pass caches rows into wrapping slots, the field goes wide at once
+    ("wheel20000", lambda: polar_arrays(20000, 2), [[0]]),
     ("ico5", lambda: g.icosphere_arrays(5), [[0], [5, 700, 9000]]),
     ("noisy_ico6", lambda: g.noisy_icosphere_arrays(6, 2e-3, 1), [[0], [1, 20000, 33333, 40000]]),
     ("torus64x48", lambda: g.torus_arrays(64, 48), [[0], [17, 1500, 3000]]),
